@@ -1,0 +1,118 @@
+/* bbcodec.h -- C ABI of the B200-native BBC1 activation codec.
+ *
+ * The drop-in boundary for the reference's hot path (BloomBee `beeplan` codec):
+ * plain pointers, sizes and a cudaStream_t passed as void*; no C++ or torch
+ * types.  The C++ drop-in (include/beeplan/codec.hpp, same declarations as the
+ * reference header) and the Python mirror (paper_2604_21072_b200/codec.py)
+ * both sit on top of these symbols.
+ *
+ * Reference interfaces replaced (file:line in /root/reference/proj):
+ *   bb_split / bb_split_host        byte_split              src/codec.cpp:86-99,   include/beeplan/codec.hpp:21
+ *   bb_merge / bb_merge_host        byte_merge              src/codec.cpp:101-111, include/beeplan/codec.hpp:22
+ *   bb_histogram256                 entropy_bits_per_byte's histogram  src/codec.cpp:113-125
+ *   bb_backend_encode/_decode       CodecBackend::encode/decode (ids 0 identity, 1 deflate =
+ *                                   zlib 1.3 compress2 level 6 / uncompress) src/codec.cpp:17-60
+ *   bb_compress / bb_compress_host  serialize_container(compress(stream, backend, split))
+ *                                   src/codec.cpp:127-140,163-179
+ *   bb_decompress / _host           decompress(parse_container(bytes)) src/codec.cpp:142-161,181-192
+ *   bb_compress_batch               the stage hand-off's per-micro-batch compress calls
+ *                                   src/wire.cpp:406-411,496-501 (batched into one pipeline)
+ *   bb_decompress_batch             the per-micro-batch decompress calls src/wire.cpp:484-491,581-585
+ *
+ * Status codes map 1:1 onto the reference exception types (include/beeplan/errors.hpp:40-56).
+ * All device entry points are stream-ordered; those returning a size on the host
+ * synchronize the given stream before returning.  A context is not thread-safe;
+ * use one per host thread (the C++ shim keeps a thread_local one).
+ */
+#ifndef BBCODEC_H
+#define BBCODEC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BB_OK = 0,
+  BB_ODD_LENGTH = 1,        /* beeplan::OddLength */
+  BB_LANE_MISMATCH = 2,     /* beeplan::LaneLengthMismatch */
+  BB_BACKEND_UNKNOWN = 3,   /* beeplan::BackendUnknown */
+  BB_CORRUPT_CONTAINER = 4, /* beeplan::CorruptContainer */
+  BB_ERROR = 5,             /* beeplan::Error */
+  BB_CUDA_ERROR = 6,        /* CUDA runtime failure (no reference equivalent) */
+  BB_INVALID_ARG = 7        /* caller error: null pointer / buffer too small */
+} bb_status;
+
+enum { BB_BACKEND_IDENTITY = 0, BB_BACKEND_DEFLATE = 1 };
+#define BB_CONTAINER_HEADER 31
+
+typedef struct bb_ctx bb_ctx;
+
+#if defined(__GNUC__)
+#define BB_API __attribute__((visibility("default")))
+#else
+#define BB_API
+#endif
+
+BB_API const char* bb_last_error(void);
+BB_API const char* bb_version(void);
+
+BB_API int bb_ctx_create(bb_ctx** out, int device);
+BB_API void bb_ctx_destroy(bb_ctx* ctx);
+
+/* ---- lanes (device) --------------------------------------------------- */
+BB_API int bb_split(const uint8_t* d_stream, size_t n_bytes, uint8_t* d_high, uint8_t* d_low, void* stream);
+BB_API int bb_merge(const uint8_t* d_high, const uint8_t* d_low, size_t count, uint8_t* d_stream, void* stream);
+/* 256 u64 counts, overwritten */
+BB_API int bb_histogram256(const uint8_t* d_data, size_t n, uint64_t* d_counts, void* stream);
+
+/* ---- codec (device) ---------------------------------------------------- */
+/* Upper bound on the serialized container size. */
+BB_API size_t bb_compress_bound(size_t n_bytes, int backend, int split);
+/* serialize_container(compress(d_in[0:n], backend, split)) into d_out. */
+BB_API int bb_compress(bb_ctx* ctx, const uint8_t* d_in, size_t n, int backend, int split, uint8_t* d_out,
+                size_t out_cap, size_t* out_len, void* stream);
+/* decompress(parse_container(d_in[0:n])) into d_out; *out_len = decoded bytes.
+ * With d_out == NULL only validates the header and reports the decoded size. */
+BB_API int bb_decompress(bb_ctx* ctx, const uint8_t* d_in, size_t n, uint8_t* d_out, size_t out_cap,
+                  size_t* out_len, void* stream);
+/* Many tensors (e.g. the M micro-batches of one step) through one pipeline.
+ * out_len[i] / status[i] per item; returns the first non-OK status. */
+BB_API int bb_compress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, const size_t* n, int backend,
+                      int split, uint8_t* const* d_out, const size_t* out_cap, size_t* out_len,
+                      int* status, void* stream);
+BB_API int bb_decompress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, const size_t* n,
+                        uint8_t* const* d_out, const size_t* out_cap, size_t* out_len, int* status,
+                        void* stream);
+
+/* ---- backend level (one lane; CodecBackend::encode / decode) ----------- */
+BB_API size_t bb_backend_bound(int backend, size_t n);
+BB_API int bb_backend_encode(bb_ctx* ctx, int backend, const uint8_t* d_in, size_t n, uint8_t* d_out,
+                      size_t out_cap, size_t* out_len, void* stream);
+BB_API int bb_backend_decode(bb_ctx* ctx, int backend, const uint8_t* d_in, size_t n, size_t expected,
+                      uint8_t* d_out, void* stream);
+
+/* ---- host buffers (the reference-facing Bytes -> Bytes calls) ----------
+ * H2D copy, the device pipeline, D2H copy; synchronous. */
+BB_API int bb_compress_host(bb_ctx* ctx, const uint8_t* h_in, size_t n, int backend, int split,
+                     uint8_t* h_out, size_t out_cap, size_t* out_len);
+BB_API int bb_decompress_host(bb_ctx* ctx, const uint8_t* h_in, size_t n, uint8_t* h_out, size_t out_cap,
+                       size_t* out_len);
+BB_API int bb_backend_encode_host(bb_ctx* ctx, int backend, const uint8_t* h_in, size_t n, uint8_t* h_out,
+                           size_t out_cap, size_t* out_len);
+BB_API int bb_backend_decode_host(bb_ctx* ctx, int backend, const uint8_t* h_in, size_t n, size_t expected,
+                           uint8_t* h_out);
+BB_API int bb_split_host(bb_ctx* ctx, const uint8_t* h_stream, size_t n_bytes, uint8_t* h_high, uint8_t* h_low);
+BB_API int bb_merge_host(bb_ctx* ctx, const uint8_t* h_high, const uint8_t* h_low, size_t count,
+                  uint8_t* h_stream);
+BB_API int bb_histogram256_host(bb_ctx* ctx, const uint8_t* h_data, size_t n, uint64_t* h_counts);
+
+/* ---- instrumentation ---------------------------------------------------- */
+/* Number of kernels this library launched (process-wide, monotonic). */
+BB_API uint64_t bb_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

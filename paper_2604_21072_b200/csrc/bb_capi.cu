@@ -1,0 +1,572 @@
+// C-ABI layer (include/bbcodec.h): argument checks, container header parsing,
+// error mapping, workspace management and dispatch onto the sm_100a kernels.
+//
+// Container semantics follow the reference exactly (/root/reference/proj):
+//   compress            src/codec.cpp:163-179 (backend lookup, then OddLength)
+//   serialize_container src/codec.cpp:127-140
+//   parse_container     src/codec.cpp:142-161 (truncated / magic / version / lengths)
+//   decompress          src/codec.cpp:181-192 (split: decode(high,N), decode(low,N), merge;
+//                                              raw: low blob must be empty, decode(high, 2N))
+//   deflate decode guard src/codec.cpp:30-31 (expected > blob*1040 + 1024 -> CorruptContainer)
+//   identity decode      src/codec.cpp:45-47 (size mismatch -> CorruptContainer)
+#include <cstdarg>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bb_common.cuh"
+#include "bb_kernels.h"
+
+namespace bb {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+}
+
+int Workspace::reserve(size_t bytes) {
+  used = 0;
+  if (bytes <= cap) return BB_OK;
+  if (base) cudaFree(base);
+  base = nullptr;
+  cap = 0;
+  size_t want = bytes + bytes / 8 + (1u << 20);
+  BB_CUDA_TRY(cudaMalloc(&base, want));
+  cap = want;
+  return BB_OK;
+}
+
+Workspace::~Workspace() {
+  if (base) cudaFree(base);
+}
+
+static int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return status;
+}
+
+}  // namespace bb
+
+using namespace bb;
+
+struct bb_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;  // stream for the host-buffer entry points
+  Workspace ws;                // lanes / inflate scratch
+  Workspace host_in, host_out; // device copies for the *_host calls
+  DeflateEngine* deflate = nullptr;
+  InflateEngine* inflate = nullptr;
+};
+
+namespace {
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+uint64_t rd_u64(const uint8_t* p) {
+  uint64_t v = 0;
+  for (int i = 0; i < 8; i++) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+
+struct Header {
+  int backend, split;
+  uint64_t count, hl, ll;
+};
+
+// parse_container (codec.cpp:142-161) on a host copy of the 31-byte header
+int parse_header(const uint8_t* h, uint64_t n, Header* c) {
+  if (n < BB_CONTAINER_HEADER) return fail(BB_CORRUPT_CONTAINER, "container: truncated header");
+  if (std::memcmp(h, "BBC1", 4) != 0) return fail(BB_CORRUPT_CONTAINER, "container: bad magic");
+  if (h[4] != 1) return fail(BB_CORRUPT_CONTAINER, "container: unsupported version %u", h[4]);
+  c->backend = h[5];
+  c->split = h[6] & 1;
+  c->count = rd_u64(h + 7);
+  c->hl = rd_u64(h + 15);
+  c->ll = rd_u64(h + 23);
+  uint64_t avail = n - BB_CONTAINER_HEADER;
+  if (c->hl > avail || c->ll > avail - c->hl || c->hl + c->ll != avail)
+    return fail(BB_CORRUPT_CONTAINER, "container: blob lengths do not match the payload");
+  return BB_OK;
+}
+
+// backend.decode(blob, expected) preconditions that need no decoding
+int lane_precheck(int backend, uint64_t blob, uint64_t expected) {
+  if (backend == BB_BACKEND_IDENTITY) {
+    if (blob != expected)
+      return fail(BB_CORRUPT_CONTAINER, "identity: blob length does not match the declared size");
+    return BB_OK;
+  }
+  if (expected > blob * 1040 + 1024)
+    return fail(BB_CORRUPT_CONTAINER, "deflate: declared size implausible for the blob");
+  return BB_OK;
+}
+
+int check_backend(int backend) {
+  if (backend != BB_BACKEND_IDENTITY && backend != BB_BACKEND_DEFLATE)
+    return fail(BB_BACKEND_UNKNOWN, "codec backend id %d is not registered", backend);
+  return BB_OK;
+}
+
+// Validates one container and returns its decoded size.
+int plan_decode(const Header& c, uint64_t* decoded) {
+  int rc = check_backend(c.backend);
+  if (rc) return rc;
+  if (c.split) {
+    if ((rc = lane_precheck(c.backend, c.hl, c.count))) return rc;
+    if ((rc = lane_precheck(c.backend, c.ll, c.count))) return rc;
+    *decoded = 2 * c.count;
+  } else {
+    if (c.ll != 0) return fail(BB_CORRUPT_CONTAINER, "container: raw mode must have an empty low blob");
+    uint64_t expected = c.count * 2;  // size_t arithmetic, as in the reference
+    if ((rc = lane_precheck(c.backend, c.hl, expected))) return rc;
+    *decoded = expected;
+  }
+  return BB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bb_last_error(void) { return t_err.c_str(); }
+const char* bb_version(void) { return "bbcodec-b200 0.1 (sm_100a)"; }
+uint64_t bb_kernel_launches(void) { return g_launches.load(); }
+
+int bb_ctx_create(bb_ctx** out, int device) {
+  if (!out) return fail(BB_INVALID_ARG, "null ctx pointer");
+  BB_CUDA_TRY(cudaSetDevice(device));
+  bb_ctx* c = new bb_ctx();
+  c->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(BB_CUDA_ERROR, "cudaStreamCreate: %s", cudaGetErrorString(e));
+  }
+  c->deflate = deflate_engine_create();
+  c->inflate = inflate_engine_create();
+  *out = c;
+  return BB_OK;
+}
+
+void bb_ctx_destroy(bb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  deflate_engine_destroy(c->deflate);
+  inflate_engine_destroy(c->inflate);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+int bb_split(const uint8_t* d_stream, size_t n, uint8_t* d_high, uint8_t* d_low, void* stream) {
+  if (n % 2) return fail(BB_ODD_LENGTH, "byte_split: stream length must be even, got %zu", n);
+  if (n && (!d_stream || !d_high || !d_low)) return fail(BB_INVALID_ARG, "null pointer");
+  return launch_split(d_stream, n / 2, d_high, d_low, S(stream));
+}
+
+int bb_merge(const uint8_t* d_high, const uint8_t* d_low, size_t count, uint8_t* d_out, void* stream) {
+  if (count && (!d_high || !d_low || !d_out)) return fail(BB_INVALID_ARG, "null pointer");
+  return launch_merge(d_high, d_low, count, d_out, S(stream));
+}
+
+int bb_histogram256(const uint8_t* d, size_t n, uint64_t* d_counts, void* stream) {
+  if (!d_counts || (n && !d)) return fail(BB_INVALID_ARG, "null pointer");
+  return launch_hist256(d, n, reinterpret_cast<unsigned long long*>(d_counts), S(stream));
+}
+
+size_t bb_backend_bound(int backend, size_t n) {
+  // zlib compressBound (compress.c) for deflate; identity is a copy
+  return backend == BB_BACKEND_DEFLATE ? n + (n >> 12) + (n >> 14) + (n >> 25) + 13 : n;
+}
+
+size_t bb_compress_bound(size_t n, int backend, int split) {
+  if (split) return BB_CONTAINER_HEADER + 2 * bb_backend_bound(backend, n / 2);
+  return BB_CONTAINER_HEADER + bb_backend_bound(backend, n);
+}
+
+int bb_compress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, const size_t* n, int backend,
+                      int split, uint8_t* const* d_out, const size_t* out_cap, size_t* out_len,
+                      int* status, void* stream) {
+  if (!ctx || count < 0) return fail(BB_INVALID_ARG, "bad arguments");
+  cudaStream_t st = S(stream);
+  int first = BB_OK;
+  int rc = check_backend(backend);
+  std::vector<int> st_local(count > 0 ? count : 1);
+  int* stv = status ? status : st_local.data();
+  for (int i = 0; i < count; i++) {
+    stv[i] = rc;
+    out_len[i] = 0;
+  }
+  if (rc) return rc;
+  std::vector<LaneJob> lanes;
+  std::vector<ContainerJob> cons;
+  std::vector<int> con_item;
+  size_t lane_bytes = 0;
+  for (int i = 0; i < count; i++) {
+    if (n[i] % 2) {
+      stv[i] = fail(BB_ODD_LENGTH, "compress: FP16 stream length must be even");
+      continue;
+    }
+    if (backend == BB_BACKEND_DEFLATE && split) lane_bytes += ((n[i] + 255) & ~size_t(255)) + 256;
+  }
+  if (lane_bytes) {
+    int r = ctx->ws.reserve(lane_bytes + 4096);
+    if (r) return r;
+  }
+  for (int i = 0; i < count; i++) {
+    if (stv[i]) continue;
+    if (backend == BB_BACKEND_IDENTITY) {
+      if (out_cap[i] < BB_CONTAINER_HEADER + n[i]) {
+        stv[i] = fail(BB_INVALID_ARG, "output buffer too small");
+        continue;
+      }
+      int r = launch_identity_container(d_in[i], n[i], split, d_out[i], st);
+      if (r) return r;
+      out_len[i] = BB_CONTAINER_HEADER + n[i];
+      continue;
+    }
+    int ci = (int)cons.size();
+    cons.push_back(ContainerJob{d_out[i], out_cap[i], n[i] / 2, split});
+    con_item.push_back(i);
+    if (split) {
+      uint64_t N = n[i] / 2;
+      uint8_t* hi = ctx->ws.take<uint8_t>(N + 16);
+      uint8_t* lo = ctx->ws.take<uint8_t>(N + 16);
+      int r = launch_split(d_in[i], N, hi, lo, st);
+      if (r) return r;
+      lanes.push_back(LaneJob{hi, N, ci, 0});
+      lanes.push_back(LaneJob{lo, N, ci, 1});
+    } else {
+      lanes.push_back(LaneJob{d_in[i], n[i], ci, 0});
+    }
+  }
+  if (!cons.empty()) {
+    std::vector<uint64_t> clen(cons.size());
+    std::vector<int> cst(cons.size());
+    int r = deflate_containers(ctx->deflate, lanes, cons, st, clen.data(), cst.data());
+    if (r) return r;
+    for (size_t k = 0; k < cons.size(); k++) {
+      int i = con_item[k];
+      stv[i] = cst[k];
+      out_len[i] = clen[k];
+      if (cst[k]) fail(cst[k], "output buffer too small for the compressed container");
+    }
+  }
+  for (int i = 0; i < count; i++)
+    if (stv[i] && !first) first = stv[i];
+  return first;
+}
+
+int bb_compress(bb_ctx* ctx, const uint8_t* d_in, size_t n, int backend, int split, uint8_t* d_out,
+                size_t out_cap, size_t* out_len, void* stream) {
+  int status = 0;
+  size_t len = 0;
+  int rc = bb_compress_batch(ctx, 1, &d_in, &n, backend, split, &d_out, &out_cap, &len, &status, stream);
+  if (out_len) *out_len = len;
+  return rc;
+}
+
+int bb_decompress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, const size_t* n,
+                        uint8_t* const* d_out, const size_t* out_cap, size_t* out_len, int* status,
+                        void* stream) {
+  if (!ctx || count < 0) return fail(BB_INVALID_ARG, "bad arguments");
+  cudaStream_t st = S(stream);
+  std::vector<int> st_local(count > 0 ? count : 1);
+  int* stv = status ? status : st_local.data();
+  // 1. headers to the host (parse_container runs host-side on 31 bytes)
+  std::vector<uint8_t> hdr((size_t)count * BB_CONTAINER_HEADER + 1);
+  for (int i = 0; i < count; i++) {
+    out_len[i] = 0;
+    if (n[i] >= BB_CONTAINER_HEADER)
+      BB_CUDA_TRY(cudaMemcpyAsync(hdr.data() + (size_t)i * BB_CONTAINER_HEADER, d_in[i],
+                                  BB_CONTAINER_HEADER, cudaMemcpyDeviceToHost, st));
+  }
+  BB_CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<Header> H(count > 0 ? count : 1);
+  std::vector<uint64_t> dec(count > 0 ? count : 1, 0);
+  size_t scratch = 0;
+  for (int i = 0; i < count; i++) {
+    stv[i] = parse_header(hdr.data() + (size_t)i * BB_CONTAINER_HEADER, n[i], &H[i]);
+    if (!stv[i]) stv[i] = plan_decode(H[i], &dec[i]);
+    if (!stv[i]) {
+      out_len[i] = dec[i];
+      if (d_out && d_out[i] && out_cap[i] < dec[i]) stv[i] = fail(BB_INVALID_ARG, "output buffer too small");
+      if (!stv[i] && H[i].backend == BB_BACKEND_DEFLATE && H[i].split)
+        scratch += 2 * (((H[i].count + 255) & ~uint64_t(255)) + 256);
+    }
+  }
+  if (!d_out) {
+    int first = BB_OK;
+    for (int i = 0; i < count; i++)
+      if (stv[i] && !first) first = stv[i];
+    return first;
+  }
+  if (scratch) {
+    int r = ctx->ws.reserve(scratch + 4096);
+    if (r) return r;
+  }
+  // 2. decode
+  std::vector<InflateJob> jobs;
+  std::vector<int> job_item;
+  struct MergeTask {
+    int item;
+    uint8_t *hi, *lo;
+  };
+  std::vector<MergeTask> merges;
+  for (int i = 0; i < count; i++) {
+    if (stv[i]) continue;
+    const Header& c = H[i];
+    const uint8_t* hb = d_in[i] + BB_CONTAINER_HEADER;
+    const uint8_t* lb = hb + c.hl;
+    if (c.backend == BB_BACKEND_IDENTITY) {
+      if (c.split) {
+        int r = launch_merge(hb, lb, c.count, d_out[i], st);
+        if (r) return r;
+      } else if (dec[i]) {
+        BB_CUDA_TRY(cudaMemcpyAsync(d_out[i], hb, dec[i], cudaMemcpyDeviceToDevice, st));
+      }
+      continue;
+    }
+    if (c.split) {
+      uint8_t* hi = ctx->ws.take<uint8_t>(c.count + 16);
+      uint8_t* lo = ctx->ws.take<uint8_t>(c.count + 16);
+      jobs.push_back(InflateJob{hb, c.hl, hi, c.count});
+      job_item.push_back(i);
+      jobs.push_back(InflateJob{lb, c.ll, lo, c.count});
+      job_item.push_back(i);
+      merges.push_back(MergeTask{i, hi, lo});
+    } else {
+      jobs.push_back(InflateJob{hb, c.hl, d_out[i], dec[i]});
+      job_item.push_back(i);
+    }
+  }
+  if (!jobs.empty()) {
+    std::vector<int> js(jobs.size());
+    int r = inflate_lanes(ctx->inflate, jobs, st, js.data());
+    if (r) return r;
+    for (size_t k = 0; k < jobs.size(); k++)
+      if (js[k] && !stv[job_item[k]])
+        stv[job_item[k]] = fail(js[k], "deflate: blob does not inflate to the declared size");
+    for (const MergeTask& m : merges) {
+      if (stv[m.item]) continue;
+      int r2 = launch_merge(m.hi, m.lo, H[m.item].count, d_out[m.item], st);
+      if (r2) return r2;
+    }
+  }
+  int first = BB_OK;
+  for (int i = 0; i < count; i++) {
+    if (stv[i]) out_len[i] = 0;
+    if (stv[i] && !first) first = stv[i];
+  }
+  return first;
+}
+
+int bb_decompress(bb_ctx* ctx, const uint8_t* d_in, size_t n, uint8_t* d_out, size_t out_cap,
+                  size_t* out_len, void* stream) {
+  int status = 0;
+  size_t len = 0;
+  uint8_t* outs[1] = {d_out};
+  int rc = bb_decompress_batch(ctx, 1, &d_in, &n, d_out ? outs : nullptr, &out_cap, &len, &status, stream);
+  if (out_len) *out_len = len;
+  return rc;
+}
+
+int bb_backend_encode(bb_ctx* ctx, int backend, const uint8_t* d_in, size_t n, uint8_t* d_out,
+                      size_t out_cap, size_t* out_len, void* stream) {
+  int rc = check_backend(backend);
+  if (rc) return rc;
+  if (!ctx) return fail(BB_INVALID_ARG, "null ctx");
+  cudaStream_t st = S(stream);
+  if (backend == BB_BACKEND_IDENTITY) {
+    if (out_cap < n) return fail(BB_INVALID_ARG, "output buffer too small");
+    if (n) BB_CUDA_TRY(cudaMemcpyAsync(d_out, d_in, n, cudaMemcpyDeviceToDevice, st));
+    *out_len = n;
+    return BB_OK;
+  }
+  // a "container" with no header: the blob goes straight to d_out
+  std::vector<LaneJob> lanes{LaneJob{d_in, n, 0, 0}};
+  std::vector<ContainerJob> cons{ContainerJob{d_out, out_cap, n, -1}};
+  uint64_t len = 0;
+  int cst = 0;
+  rc = deflate_containers(ctx->deflate, lanes, cons, st, &len, &cst);
+  if (rc) return rc;
+  if (cst) return fail(cst, "output buffer too small");
+  *out_len = len;
+  return BB_OK;
+}
+
+int bb_backend_decode(bb_ctx* ctx, int backend, const uint8_t* d_in, size_t n, size_t expected,
+                      uint8_t* d_out, void* stream) {
+  int rc = check_backend(backend);
+  if (rc) return rc;
+  if ((rc = lane_precheck(backend, n, expected))) return rc;
+  cudaStream_t st = S(stream);
+  if (backend == BB_BACKEND_IDENTITY) {
+    if (n) BB_CUDA_TRY(cudaMemcpyAsync(d_out, d_in, n, cudaMemcpyDeviceToDevice, st));
+    return BB_OK;
+  }
+  std::vector<InflateJob> jobs{InflateJob{d_in, n, d_out, expected}};
+  int js = 0;
+  rc = inflate_lanes(ctx->inflate, jobs, st, &js);
+  if (rc) return rc;
+  if (js) return fail(js, "deflate: blob does not inflate to the declared size");
+  return BB_OK;
+}
+
+// ---- host-buffer entry points --------------------------------------------
+
+static int to_device(bb_ctx* c, Workspace& w, const uint8_t* h, size_t n, uint8_t** d) {
+  int r = w.reserve(n + 64);
+  if (r) return r;
+  *d = static_cast<uint8_t*>(w.base);
+  if (n) BB_CUDA_TRY(cudaMemcpyAsync(*d, h, n, cudaMemcpyHostToDevice, c->own));
+  return BB_OK;
+}
+
+int bb_compress_host(bb_ctx* c, const uint8_t* h_in, size_t n, int backend, int split, uint8_t* h_out,
+                     size_t out_cap, size_t* out_len) {
+  if (!c) return fail(BB_INVALID_ARG, "null ctx");
+  BB_CUDA_TRY(cudaSetDevice(c->device));
+  uint8_t *din, *dout;
+  int rc = to_device(c, c->host_in, h_in, n, &din);
+  if (rc) return rc;
+  size_t bound = bb_compress_bound(n, backend, split);
+  if ((rc = c->host_out.reserve(bound + 64))) return rc;
+  dout = static_cast<uint8_t*>(c->host_out.base);
+  size_t len = 0;
+  rc = bb_compress(c, din, n, backend, split, dout, bound, &len, c->own);
+  if (rc) return rc;
+  if (len > out_cap) return fail(BB_INVALID_ARG, "output buffer too small");
+  if (len) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, len, cudaMemcpyDeviceToHost, c->own));
+  BB_CUDA_TRY(cudaStreamSynchronize(c->own));
+  *out_len = len;
+  return BB_OK;
+}
+
+int bb_decompress_host(bb_ctx* c, const uint8_t* h_in, size_t n, uint8_t* h_out, size_t out_cap,
+                       size_t* out_len) {
+  if (!c) return fail(BB_INVALID_ARG, "null ctx");
+  BB_CUDA_TRY(cudaSetDevice(c->device));
+  uint8_t* din;
+  int rc = to_device(c, c->host_in, h_in, n, &din);
+  if (rc) return rc;
+  size_t need = 0;
+  rc = bb_decompress(c, din, n, nullptr, 0, &need, c->own);
+  if (rc) return rc;
+  if (!h_out) {
+    *out_len = need;
+    return BB_OK;
+  }
+  if (need > out_cap) return fail(BB_INVALID_ARG, "output buffer too small");
+  if ((rc = c->host_out.reserve(need + 64))) return rc;
+  uint8_t* dout = static_cast<uint8_t*>(c->host_out.base);
+  size_t len = 0;
+  rc = bb_decompress(c, din, n, dout, need, &len, c->own);
+  if (rc) return rc;
+  if (len) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, len, cudaMemcpyDeviceToHost, c->own));
+  BB_CUDA_TRY(cudaStreamSynchronize(c->own));
+  *out_len = len;
+  return BB_OK;
+}
+
+int bb_backend_encode_host(bb_ctx* c, int backend, const uint8_t* h_in, size_t n, uint8_t* h_out,
+                           size_t out_cap, size_t* out_len) {
+  if (!c) return fail(BB_INVALID_ARG, "null ctx");
+  int rc = check_backend(backend);
+  if (rc) return rc;
+  BB_CUDA_TRY(cudaSetDevice(c->device));
+  uint8_t* din;
+  if ((rc = to_device(c, c->host_in, h_in, n, &din))) return rc;
+  size_t bound = bb_backend_bound(backend, n);
+  if ((rc = c->host_out.reserve(bound + 64))) return rc;
+  uint8_t* dout = static_cast<uint8_t*>(c->host_out.base);
+  size_t len = 0;
+  if ((rc = bb_backend_encode(c, backend, din, n, dout, bound, &len, c->own))) return rc;
+  if (len > out_cap) return fail(BB_INVALID_ARG, "output buffer too small");
+  if (len) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, len, cudaMemcpyDeviceToHost, c->own));
+  BB_CUDA_TRY(cudaStreamSynchronize(c->own));
+  *out_len = len;
+  return BB_OK;
+}
+
+int bb_backend_decode_host(bb_ctx* c, int backend, const uint8_t* h_in, size_t n, size_t expected,
+                           uint8_t* h_out) {
+  if (!c) return fail(BB_INVALID_ARG, "null ctx");
+  int rc = check_backend(backend);
+  if (rc) return rc;
+  if ((rc = lane_precheck(backend, n, expected))) return rc;
+  BB_CUDA_TRY(cudaSetDevice(c->device));
+  uint8_t* din;
+  if ((rc = to_device(c, c->host_in, h_in, n, &din))) return rc;
+  if ((rc = c->host_out.reserve(expected + 64))) return rc;
+  uint8_t* dout = static_cast<uint8_t*>(c->host_out.base);
+  if ((rc = bb_backend_decode(c, backend, din, n, expected, dout, c->own))) return rc;
+  if (expected) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, expected, cudaMemcpyDeviceToHost, c->own));
+  BB_CUDA_TRY(cudaStreamSynchronize(c->own));
+  return BB_OK;
+}
+
+int bb_split_host(bb_ctx* c, const uint8_t* h_stream, size_t n, uint8_t* h_high, uint8_t* h_low) {
+  if (!c) return fail(BB_INVALID_ARG, "null ctx");
+  if (n % 2) return fail(BB_ODD_LENGTH, "byte_split: stream length must be even, got %zu", n);
+  BB_CUDA_TRY(cudaSetDevice(c->device));
+  uint8_t* din;
+  int rc = to_device(c, c->host_in, h_stream, n, &din);
+  if (rc) return rc;
+  if ((rc = c->host_out.reserve(n + 64))) return rc;
+  uint8_t* hi = static_cast<uint8_t*>(c->host_out.base);
+  uint8_t* lo = hi + ((n / 2 + 15) & ~size_t(15));
+  if ((rc = launch_split(din, n / 2, hi, lo, c->own))) return rc;
+  if (n) {
+    BB_CUDA_TRY(cudaMemcpyAsync(h_high, hi, n / 2, cudaMemcpyDeviceToHost, c->own));
+    BB_CUDA_TRY(cudaMemcpyAsync(h_low, lo, n / 2, cudaMemcpyDeviceToHost, c->own));
+  }
+  BB_CUDA_TRY(cudaStreamSynchronize(c->own));
+  return BB_OK;
+}
+
+int bb_merge_host(bb_ctx* c, const uint8_t* h_high, const uint8_t* h_low, size_t count, uint8_t* h_out) {
+  if (!c) return fail(BB_INVALID_ARG, "null ctx");
+  BB_CUDA_TRY(cudaSetDevice(c->device));
+  int rc = c->host_in.reserve(2 * count + 64);
+  if (rc) return rc;
+  uint8_t* hi = static_cast<uint8_t*>(c->host_in.base);
+  uint8_t* lo = hi + ((count + 15) & ~size_t(15));
+  if (count) {
+    BB_CUDA_TRY(cudaMemcpyAsync(hi, h_high, count, cudaMemcpyHostToDevice, c->own));
+    BB_CUDA_TRY(cudaMemcpyAsync(lo, h_low, count, cudaMemcpyHostToDevice, c->own));
+  }
+  if ((rc = c->host_out.reserve(2 * count + 64))) return rc;
+  uint8_t* dout = static_cast<uint8_t*>(c->host_out.base);
+  if ((rc = launch_merge(hi, lo, count, dout, c->own))) return rc;
+  if (count) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, 2 * count, cudaMemcpyDeviceToHost, c->own));
+  BB_CUDA_TRY(cudaStreamSynchronize(c->own));
+  return BB_OK;
+}
+
+int bb_histogram256_host(bb_ctx* c, const uint8_t* h_data, size_t n, uint64_t* h_counts) {
+  if (!c) return fail(BB_INVALID_ARG, "null ctx");
+  BB_CUDA_TRY(cudaSetDevice(c->device));
+  uint8_t* din;
+  int rc = to_device(c, c->host_in, h_data, n, &din);
+  if (rc) return rc;
+  if ((rc = c->host_out.reserve(256 * 8 + 64))) return rc;
+  unsigned long long* cnt = static_cast<unsigned long long*>(c->host_out.base);
+  if ((rc = launch_hist256(din, n, cnt, c->own))) return rc;
+  BB_CUDA_TRY(cudaMemcpyAsync(h_counts, cnt, 256 * 8, cudaMemcpyDeviceToHost, c->own));
+  BB_CUDA_TRY(cudaStreamSynchronize(c->own));
+  return BB_OK;
+}
+
+}  // extern "C"
