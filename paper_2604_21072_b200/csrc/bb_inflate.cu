@@ -1,12 +1,391 @@
-// placeholder: replaced by the GPU inflater
+// The deflate backend's decode: zlib 1.3 uncompress() semantics on sm_100a.
+//
+// Reference: deflate_decode (/root/reference/proj/src/codec.cpp:27-38) =
+// uncompress(out, &expected, blob) followed by a size check.  zlib (third-party,
+// pinned 1.3) accepts a stream iff the header, every block, and the Adler-32
+// trailer are valid and the output fits destLen; trailing bytes are ignored;
+// destLen == 0 is served by a 1-byte scratch buffer.  The CPU restatement of
+// those rules is oracle/inflate.c; this file implements the same rules.
+//
+// This is the exact, sequential-per-stream decoder (one CTA per lane: one thread
+// walks the bit stream with shared-memory Huffman tables, then the whole CTA
+// verifies the Adler-32).  It defines correctness and error parity for every
+// input.
+#include <cstring>
+#include <vector>
+
 #include "bb_common.cuh"
 #include "bb_kernels.h"
+
 namespace bb {
-struct InflateEngine {};
-InflateEngine* inflate_engine_create() { return new InflateEngine(); }
-void inflate_engine_destroy(InflateEngine* e) { delete e; }
-int inflate_lanes(InflateEngine*, const std::vector<InflateJob>&, cudaStream_t, int*) {
-  set_error("inflate not built yet");
-  return BB_ERROR;
+
+namespace {
+
+constexpr int FAST_BITS = 10;
+
+struct Huff {
+  int16_t count[16];
+  int16_t symbol[320];
+  uint16_t fast[1 << FAST_BITS];  // (symbol << 4) | len, 0 = slow path
+  int max;
+};
+
+__constant__ uint16_t c_lbase[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
+                                     31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t c_lext[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t c_dbase[30] = {1,    2,    3,    4,    5,    7,    9,    13,    17,    25,
+                                     33,   49,   65,   97,   129,  193,  257,  385,   513,   769,
+                                     1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ uint8_t c_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+__constant__ uint8_t c_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+
+enum { T_CODES = 0, T_LENS = 1, T_DISTS = 2 };
+
+// inftrees.c inflate_table validity + canonical tables
+__device__ int build(Huff* h, const uint16_t* lens, int n, int type) {
+  int16_t offs[16];
+  for (int i = 0; i < 16; i++) h->count[i] = 0;
+  for (int s = 0; s < n; s++) h->count[lens[s]]++;
+  int max = 15;
+  while (max >= 1 && h->count[max] == 0) max--;
+  h->max = max;
+  for (int i = 0; i < (1 << FAST_BITS); i++) h->fast[i] = 0;
+  if (max == 0) return 0;
+  int left = 1;
+  for (int len = 1; len <= 15; len++) {
+    left <<= 1;
+    left -= h->count[len];
+    if (left < 0) return -1;
+  }
+  if (left > 0 && (type == T_CODES || max != 1)) return -1;
+  offs[1] = 0;
+  for (int len = 1; len < 15; len++) offs[len + 1] = (int16_t)(offs[len] + h->count[len]);
+  for (int s = 0; s < n; s++)
+    if (lens[s] != 0) h->symbol[offs[lens[s]]++] = (int16_t)s;
+  // fast table: canonical codes are assigned in (len, symbol) order
+  int code = 0, idx = 0;
+  for (int len = 1; len <= FAST_BITS && len <= max; len++) {
+    for (int k = 0; k < h->count[len]; k++, idx++, code++) {
+      int sym = h->symbol[idx];
+      int rev = __brev((unsigned)code) >> (32 - len);
+      for (int fill = rev; fill < (1 << FAST_BITS); fill += 1 << len)
+        h->fast[fill] = (uint16_t)((sym << 4) | len);
+    }
+    code <<= 1;
+  }
+  return 0;
 }
+
+struct Bits {
+  const uint8_t* in;
+  uint64_t n, pos;
+  uint64_t hold;
+  int bits;
+  __device__ __forceinline__ void fill() {
+    while (bits <= 56 && pos < n) {
+      hold |= (uint64_t)in[pos++] << bits;
+      bits += 8;
+    }
+  }
+  __device__ __forceinline__ bool need(int k) {
+    if (bits < k) fill();
+    return bits >= k;
+  }
+  __device__ __forceinline__ uint32_t take(int k) {
+    uint32_t v = (uint32_t)(hold & ((1ull << k) - 1));
+    hold >>= k;
+    bits -= k;
+    return v;
+  }
+};
+
+// -1 invalid code, -2 out of input
+__device__ __forceinline__ int decode(Bits& b, const Huff* h) {
+  if (h->max == 0) {
+    if (!b.need(1)) return -2;
+    return -1;
+  }
+  b.fill();
+  if (b.bits >= FAST_BITS || b.bits >= h->max) {
+    uint32_t e = h->fast[b.hold & ((1u << FAST_BITS) - 1)];
+    if (e && (int)(e & 15) <= b.bits) {
+      b.take(e & 15);
+      return e >> 4;
+    }
+  }
+  int code = 0, first = 0, index = 0;
+  for (int len = 1; len <= 15; len++) {
+    if (!b.need(1)) return -2;
+    code |= (int)b.take(1);
+    int count = h->count[len];
+    if (code - count < first) return h->symbol[index + (code - first)];
+    index += count;
+    first += count;
+    first <<= 1;
+    code <<= 1;
+    if (len >= h->max) return -1;
+  }
+  return -1;
+}
+
+struct Sink {
+  uint8_t* out;
+  uint64_t lim, total;
+  uint8_t scratch;
+  __device__ __forceinline__ bool put(uint8_t v) {
+    if (total >= lim) return false;
+    out[total++] = v;
+    return true;
+  }
+};
+
+struct InflSmem {
+  Huff lh, dh, ch;
+  uint16_t lens[320];
+  int status;
+  uint64_t total;
+  uint32_t want_adler;
+};
+
+__device__ int codes(Bits& b, Sink& s, const Huff* lh, const Huff* dh) {
+  for (;;) {
+    int sym = decode(b, lh);
+    if (sym < 0) return -1;
+    if (sym < 256) {
+      if (!s.put((uint8_t)sym)) return -1;
+    } else if (sym == 256) {
+      return 0;
+    } else {
+      sym -= 257;
+      if (sym >= 29) return -1;
+      if (!b.need(c_lext[sym])) return -1;
+      uint32_t len = c_lbase[sym] + b.take(c_lext[sym]);
+      int ds = decode(b, dh);
+      if (ds < 0 || ds >= 30) return -1;
+      if (!b.need(c_dext[ds])) return -1;
+      uint64_t dist = c_dbase[ds] + b.take(c_dext[ds]);
+      if (dist > s.total) return -1;
+      if (s.total + len > s.lim) return -1;
+      for (uint32_t i = 0; i < len; i++) s.out[s.total + i] = s.out[s.total + i - dist];
+      s.total += len;
+    }
+  }
+}
+
+// returns 0 on a complete valid stream (adler not yet checked)
+__device__ int inflate_stream(const uint8_t* in, uint64_t n, Sink& s, InflSmem& S) {
+  Bits b{in, n, 0, 0, 0};
+  if (n < 2) return -5;
+  uint32_t cmf = in[0], flg = in[1];
+  b.pos = 2;
+  if (((cmf << 8) + flg) % 31 != 0) return -3;
+  if ((cmf & 0x0f) != 8) return -3;
+  if ((cmf >> 4) + 8 > 15) return -3;
+  if (flg & 0x20) return -3;
+  int last;
+  do {
+    if (!b.need(3)) return -5;
+    last = (int)b.take(1);
+    uint32_t type = b.take(2);
+    if (type == 0) {
+      b.take(b.bits & 7);
+      if (!b.need(32)) return -5;
+      uint32_t len = b.take(16), nlen = b.take(16);
+      if (len != (~nlen & 0xffff)) return -3;
+      while (len && b.bits) {
+        if (!s.put((uint8_t)b.take(8))) return -5;
+        len--;
+      }
+      if (b.pos + len > n) return -5;
+      if (s.total + len > s.lim) return -5;
+      for (uint32_t i = 0; i < len; i++) s.out[s.total + i] = in[b.pos + i];
+      s.total += len;
+      b.pos += len;
+    } else if (type == 1) {
+      for (int i = 0; i < 288; i++) S.lens[i] = i < 144 ? 8 : i < 256 ? 9 : i < 280 ? 7 : 8;
+      build(&S.lh, S.lens, 288, T_LENS);
+      for (int i = 0; i < 32; i++) S.lens[i] = 5;
+      build(&S.dh, S.lens, 32, T_DISTS);
+      if (codes(b, s, &S.lh, &S.dh)) return -3;
+    } else if (type == 2) {
+      if (!b.need(14)) return -5;
+      int nlen = (int)b.take(5) + 257, ndist = (int)b.take(5) + 1, ncode = (int)b.take(4) + 4;
+      if (nlen > 286 || ndist > 30) return -3;
+      for (int i = 0; i < 320; i++) S.lens[i] = 0;
+      for (int i = 0; i < ncode; i++) {
+        if (!b.need(3)) return -5;
+        S.lens[c_order[i]] = (uint16_t)b.take(3);
+      }
+      if (build(&S.ch, S.lens, 19, T_CODES)) return -3;
+      int have = 0;
+      for (int i = 0; i < 320; i++) S.lens[i] = 0;
+      while (have < nlen + ndist) {
+        int sym;
+        if (S.ch.max == 0) {
+          if (!b.need(1)) return -5;
+          b.take(1);
+          sym = 0;
+        } else {
+          sym = decode(b, &S.ch);
+          if (sym == -2) return -5;
+          if (sym < 0) return -3;
+        }
+        if (sym < 16) {
+          S.lens[have++] = (uint16_t)sym;
+        } else {
+          uint32_t len = 0, copy;
+          if (sym == 16) {
+            if (have == 0) return -3;
+            len = S.lens[have - 1];
+            if (!b.need(2)) return -5;
+            copy = 3 + b.take(2);
+          } else if (sym == 17) {
+            if (!b.need(3)) return -5;
+            copy = 3 + b.take(3);
+          } else {
+            if (!b.need(7)) return -5;
+            copy = 11 + b.take(7);
+          }
+          if (have + (int)copy > nlen + ndist) return -3;
+          while (copy--) S.lens[have++] = (uint16_t)len;
+        }
+      }
+      if (S.lens[256] == 0) return -3;
+      if (build(&S.lh, S.lens, nlen, T_LENS)) return -3;
+      if (build(&S.dh, S.lens + nlen, ndist, T_DISTS)) return -3;
+      if (codes(b, s, &S.lh, &S.dh)) return -3;
+    } else {
+      return -3;
+    }
+  } while (!last);
+  b.take(b.bits & 7);
+  if (!b.need(32)) return -5;
+  uint32_t b0 = b.take(8), b1 = b.take(8), b2 = b.take(8), b3 = b.take(8);
+  S.want_adler = (b0 << 24) | (b1 << 16) | (b2 << 8) | b3;
+  return 0;
+}
+
+constexpr uint32_t MOD = 65521;
+
+struct Job {
+  const uint8_t* src;
+  uint64_t n;
+  uint8_t* dst;
+  uint64_t expected;
+};
+
+__global__ void __launch_bounds__(256) k_inflate_seq(const Job* __restrict__ jobs, int* __restrict__ status) {
+  __shared__ InflSmem S;
+  __shared__ uint32_t wa[8], wb[8];
+  __shared__ uint64_t wm[8];
+  const Job J = jobs[blockIdx.x];
+  if (threadIdx.x == 0) {
+    Sink s;
+    s.lim = J.expected ? J.expected : 1;
+    s.total = 0;
+    s.out = J.expected ? J.dst : &s.scratch;
+    int rc = inflate_stream(J.src, J.n, s, S);
+    if (rc == 0 && J.expected && s.total != J.expected) rc = -3;  // short output
+    if (rc == 0 && !J.expected) {
+      // uncompress2 with destLen 0: <= 1 byte lands in scratch; check it here
+      uint32_t a = 1, bsum = 0;
+      if (s.total) {
+        a = (1 + s.scratch) % MOD;
+        bsum = a;
+      }
+      if (((bsum << 16) | a) != S.want_adler) rc = -3;
+      S.total = 0;
+    } else {
+      S.total = s.total;
+    }
+    S.status = rc;
+  }
+  __syncthreads();
+  if (S.status != 0 || J.expected == 0) {
+    if (threadIdx.x == 0) status[blockIdx.x] = S.status == 0 ? BB_OK : BB_CORRUPT_CONTAINER;
+    return;
+  }
+  // Adler-32 of the output: ordered (A, B, m) reduction, 256 threads
+  const uint64_t n = S.total;
+  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t c0 = min((uint64_t)threadIdx.x * per, n), c1 = min(c0 + per, n);
+  uint64_t A = 0, B = 0;
+  for (uint64_t i = c0; i < c1; i++) {
+    uint32_t x = J.dst[i];
+    A += x;
+    B += A;
+    if (((i - c0) & 4095) == 4095) A %= MOD, B %= MOD;
+  }
+  A %= MOD;
+  B %= MOD;
+  uint64_t m = c1 - c0;
+  // B here is sum of prefix sums = sum (m - j) x_j
+  for (int off = 1; off < 32; off <<= 1) {
+    uint64_t rA = __shfl_down_sync(0xffffffffu, A, off);
+    uint64_t rB = __shfl_down_sync(0xffffffffu, B, off);
+    uint64_t rm = __shfl_down_sync(0xffffffffu, m, off);
+    int lane = threadIdx.x & 31;
+    if (lane + off < 32 && (lane & (2 * off - 1)) == 0) {
+      B = (B + rB + (rm % MOD) * A) % MOD;
+      A = (A + rA) % MOD;
+      m += rm;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    wa[threadIdx.x >> 5] = (uint32_t)A;
+    wb[threadIdx.x >> 5] = (uint32_t)B;
+    wm[threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t TA = 0, TB = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); w++) {
+      TB = (TB + wb[w] + (wm[w] % MOD) * TA) % MOD;
+      TA = (TA + wa[w]) % MOD;
+    }
+    uint32_t a = (uint32_t)((1 + TA) % MOD);
+    uint32_t bb = (uint32_t)((n % MOD + TB) % MOD);
+    status[blockIdx.x] = ((bb << 16) | a) == S.want_adler ? BB_OK : BB_CORRUPT_CONTAINER;
+  }
+}
+
+}  // namespace
+
+struct InflateEngine {
+  Workspace ws;
+  int* h_status = nullptr;
+  size_t h_cap = 0;
+};
+
+InflateEngine* inflate_engine_create() { return new InflateEngine(); }
+
+void inflate_engine_destroy(InflateEngine* e) {
+  if (!e) return;
+  if (e->h_status) cudaFreeHost(e->h_status);
+  delete e;
+}
+
+int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStream_t st, int* status) {
+  const int nj = (int)jobs.size();
+  if (nj == 0) return BB_OK;
+  int rc = e->ws.reserve(sizeof(Job) * nj + sizeof(int) * nj + 1024);
+  if (rc) return rc;
+  Job* d_jobs = e->ws.take<Job>(nj);
+  int* d_status = e->ws.take<int>(nj);
+  std::vector<Job> h(nj);
+  for (int i = 0; i < nj; i++) h[i] = Job{jobs[i].src, jobs[i].n, jobs[i].dst, jobs[i].expected};
+  if ((size_t)nj > e->h_cap) {
+    if (e->h_status) cudaFreeHost(e->h_status);
+    BB_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&e->h_status), sizeof(int) * nj, cudaHostAllocDefault));
+    e->h_cap = nj;
+  }
+  BB_CUDA_TRY(cudaMemcpyAsync(d_jobs, h.data(), sizeof(Job) * nj, cudaMemcpyHostToDevice, st));
+  k_inflate_seq<<<nj, 256, 0, st>>>(d_jobs, d_status);
+  BB_LAUNCH_CHECK();
+  BB_CUDA_TRY(cudaMemcpyAsync(e->h_status, d_status, sizeof(int) * nj, cudaMemcpyDeviceToHost, st));
+  BB_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < nj; i++) status[i] = e->h_status[i];
+  return BB_OK;
+}
+
 }  // namespace bb

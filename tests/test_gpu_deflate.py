@@ -106,3 +106,51 @@ def test_batch_compress_matches_single(codec, oracle):
     lens = dev.compress_batch(xs, outs)
     for s, o, n in zip(streams, outs, lens):
         assert o[:n].cpu().numpy().tobytes() == oracle.compress(s, 1, True)
+
+
+def test_lane_decode_roundtrip_and_foreign_streams(codec):
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    for data in _corpus():
+        for level in (6, 1, 9, 0):
+            blob = zlib.compress(data, level)
+            assert dec(blob, len(data)) == data
+        assert dec(zlib.compress(data, 6) + b"trailing", len(data)) == data
+
+
+def test_decode_error_parity_with_oracle(codec, oracle):
+    from oracle.oracle import OracleError
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    rng = random.Random(12)
+    base = zlib.compress(rng.randbytes(700) + bytes(300), 6)
+    for trial in range(400):
+        blob = bytearray(base)
+        for _ in range(1 + rng.randrange(6)):
+            blob[rng.randrange(len(blob))] ^= 1 << rng.randrange(8)
+        if trial % 7 == 0:
+            blob = blob[: rng.randrange(len(blob) + 1)]
+        blob = bytes(blob)
+        expected = 1000 if trial % 5 else rng.choice([0, 1, 999, 1001])
+        try:
+            want = oracle.zlib_uncompress(blob, expected)
+            want_ok = len(want) == expected
+        except OracleError:
+            want_ok = False
+        try:
+            got = dec(blob, expected)
+            got_ok = True
+        except codec.CorruptContainer:
+            got_ok = False
+        assert got_ok == want_ok, (trial, expected)
+        if got_ok:
+            assert got == want
+
+
+def test_container_roundtrip_golden_inputs(codec, golden, oracle):
+    cache = {}
+    for e in golden["entries"]:
+        if e["backend"] != 1 or e["len"] > 3_000_000:
+            continue
+        data = cache.setdefault(e["spec"], make_input(e["spec"], oracle))
+        data = data[: len(data) // 2 * 2]
+        c = oracle.compress(data, 1, e["split"])
+        assert codec.decompress_serialized(c) == data
