@@ -111,6 +111,10 @@ BB_API int bb_histogram256_host(bb_ctx* ctx, const uint8_t* h_data, size_t n, ui
 /* ---- instrumentation ---------------------------------------------------- */
 /* Number of kernels this library launched (process-wide, monotonic). */
 BB_API uint64_t bb_kernel_launches(void);
+/* Per-stage CUDA-event timing of the codec pipelines (off by default). */
+BB_API void bb_stage_timing(int enable);
+/* JSON {"stage": {"ms": total, "count": calls}, ...}; reset != 0 clears. */
+BB_API const char* bb_stage_report(int reset);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ EXPORTS = [
     "bb_decompress_batch", "bb_backend_bound", "bb_backend_encode", "bb_backend_decode",
     "bb_compress_host", "bb_decompress_host", "bb_backend_encode_host", "bb_backend_decode_host",
     "bb_split_host", "bb_merge_host", "bb_histogram256_host", "bb_kernel_launches",
+    "bb_stage_timing", "bb_stage_report",
 ]
 
 _u8p = C.c_void_p
@@ -70,6 +71,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         L.bb_merge_host.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, _sz, _u8p]
         L.bb_histogram256_host.argtypes = [C.c_void_p, C.c_char_p, _sz, _u8p]
         L.bb_kernel_launches.restype = C.c_uint64
+        L.bb_stage_timing.argtypes = [C.c_int]
+        L.bb_stage_report.restype = C.c_char_p
+        L.bb_stage_report.argtypes = [C.c_int]
         _lib = L
         return L
 
@@ -98,3 +102,12 @@ def context(device: int = 0) -> C.c_void_p:
 
 def kernel_launches() -> int:
     return int(load().bb_kernel_launches())
+
+
+def stage_timing(enable: bool) -> None:
+    load().bb_stage_timing(1 if enable else 0)
+
+
+def stage_report(reset: bool = False) -> dict:
+    import json
+    return json.loads(load().bb_stage_report(1 if reset else 0).decode())

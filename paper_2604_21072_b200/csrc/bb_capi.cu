@@ -11,6 +11,8 @@
 //   identity decode      src/codec.cpp:45-47 (size mismatch -> CorruptContainer)
 #include <cstdarg>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -20,6 +22,36 @@
 namespace bb {
 
 std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_stage_timing{0};
+
+namespace {
+struct StageAcc {
+  double ms = 0;
+  uint64_t count = 0;
+};
+std::mutex g_stage_mu;
+std::map<std::string, StageAcc> g_stage_acc;
+std::string g_stage_report;
+}  // namespace
+
+void StageTimer::finish() {
+  if (!on || n == 0) return;
+  cudaEvent_t end;
+  cudaEventCreate(&end);
+  cudaEventRecord(end, st);
+  cudaEventSynchronize(end);
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  for (int i = 0; i < n; i++) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[i], i + 1 < n ? ev[i + 1] : end);
+    StageAcc& a = g_stage_acc[names[i]];
+    a.ms += ms;
+    a.count += 1;
+    cudaEventDestroy(ev[i]);
+  }
+  cudaEventDestroy(end);
+  n = 0;
+}
 static thread_local std::string t_err;
 
 void set_error(const char* fmt, ...) {
@@ -143,6 +175,25 @@ extern "C" {
 const char* bb_last_error(void) { return t_err.c_str(); }
 const char* bb_version(void) { return "bbcodec-b200 0.1 (sm_100a)"; }
 uint64_t bb_kernel_launches(void) { return g_launches.load(); }
+
+void bb_stage_timing(int enable) { g_stage_timing.store(enable); }
+
+const char* bb_stage_report(int reset) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  std::string r = "{";
+  bool first = true;
+  for (const auto& [k, v] : g_stage_acc) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "%s\"%s\": {\"ms\": %.6f, \"count\": %llu}", first ? "" : ", ", k.c_str(), v.ms,
+             (unsigned long long)v.count);
+    r += buf;
+    first = false;
+  }
+  r += "}";
+  g_stage_report = r;
+  if (reset) g_stage_acc.clear();
+  return g_stage_report.c_str();
+}
 
 int bb_ctx_create(bb_ctx** out, int device) {
   if (!out) return fail(BB_INVALID_ARG, "null ctx pointer");

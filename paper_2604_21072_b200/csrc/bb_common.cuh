@@ -35,6 +35,26 @@ constexpr int kNumSMs = 148;  // B200
     }                                                                                           \
   } while (0)
 
+// Optional per-stage CUDA-event timing (enabled by bb_stage_timing(1)); the time
+// between consecutive marks is charged to the earlier mark's stage name.
+extern std::atomic<int> g_stage_timing;
+struct StageTimer {
+  cudaStream_t st;
+  bool on;
+  const char* names[32];
+  cudaEvent_t ev[33];
+  int n = 0;
+  explicit StageTimer(cudaStream_t s) : st(s), on(g_stage_timing.load() != 0) {}
+  void mark(const char* name) {
+    if (!on || n >= 32) return;
+    names[n] = name;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], st);
+    n++;
+  }
+  void finish();  // call after the stream is synchronized
+};
+
 inline unsigned grid_for(size_t work_items, int threads, int per_sm = 8) {
   size_t blocks = (work_items + threads - 1) / threads;
   size_t cap = (size_t)kNumSMs * per_sm;

@@ -1460,6 +1460,8 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   int* d_con_status = W.take<int>(nc);
   Adl* d_adl = W.take<Adl>(ad_work.size() + 1);
 
+  StageTimer T(st);
+  T.mark("deflate.upload");
   BB_CUDA_TRY(cudaMemcpyAsync(d_lanes, L.data(), sizeof(LaneDev) * nl, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_cons, C.data(), sizeof(ContainerDev) * nc, cudaMemcpyHostToDevice, st));
   if (!hp_work.empty())
@@ -1473,16 +1475,19 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_CUDA_TRY(cudaMemcpyAsync(d_ad_chunk0, ad_chunk0.data(), 4 * nl, cudaMemcpyHostToDevice, st));
 
   // K3, K4
+  T.mark("deflate.hash_prev");
   if (!hp_work.empty()) {
     k_hash_prev<<<(unsigned)hp_work.size(), 32, 65536, st>>>(d_lanes, d_hp, d_pd);
     BB_LAUNCH_CHECK();
   }
+  T.mark("deflate.profile");
   if (!pf_work.empty()) {
     size_t smem = ((WSIZE + PF_SEG + MAX_MATCH + 32 + 15) & ~15u) + 2 * (WSIZE + PF_SEG);
     k_profile<<<(unsigned)pf_work.size(), PF_THREADS, smem, st>>>(d_lanes, d_pf, d_pd, d_prof);
     BB_LAUNCH_CHECK();
   }
   // K5: speculative parse, then fix-up rounds until no exit state changes
+  T.mark("deflate.parse_spec");
   const unsigned pt = 64, pg = (seg_total + pt - 1) / pt;
   k_parse_spec<<<pg, pt, 0, st>>>(d_lanes, nl, d_seg_lane, seg_total, d_prof, d_spec_syms, d_state_map,
                                   d_spec_exit, d_spec_cnt, d_spec_post, sym_stride);
@@ -1501,6 +1506,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_CUDA_TRY(cudaMemsetAsync(d_conv_idx, 0, 4ull * seg_total, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_post_flag, d_spec_post, 4ull * seg_total, cudaMemcpyDeviceToDevice, st));
   if ((rc = pinned(e, 64 + 16ull * nc))) return rc;
+  T.mark("deflate.parse_fixup");
   SegExit *cur = d_exit_a, *nxt = d_exit_b;
   for (int round = 0;; round++) {
     BB_CUDA_TRY(cudaMemsetAsync(d_changed, 0, 4, st));
@@ -1519,14 +1525,17 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     }
   }
   // K6
+  T.mark("deflate.compact");
   k_seg_scan<<<nl, 256, 0, st>>>(d_lanes, d_spec_cnt, d_fix_cnt, d_conv_idx, d_post_flag, d_spec_post, d_seg_off, d_ls);
   BB_LAUNCH_CHECK();
   k_compact<<<(seg_total + 7) / 8, 256, 0, st>>>(d_lanes, d_seg_lane, seg_total, d_spec_syms, d_spec_cnt, d_fix_syms,
                                                  d_fix_cnt, d_conv_idx, d_seg_off, d_syms, sym_stride);
   BB_LAUNCH_CHECK();
+  T.mark("deflate.blocks_trees");
   BB_CUDA_TRY(cudaMemsetAsync(d_hdr, 0, (size_t)blk_total * HDR_BYTES, st));
   k_blocks<<<blk_total, BK_THREADS, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_syms, d_info, d_codes, d_hdr);
   BB_LAUNCH_CHECK();
+  T.mark("deflate.layout_zero");
   k_layout<<<(nl + 3) / 4, 128, 0, st>>>(d_lanes, nl, d_ls, d_info, d_plan, d_blob_len);
   BB_LAUNCH_CHECK();
   k_place<<<(nc + 127) / 128, 128, 0, st>>>(d_cons, nc, d_blob_len, d_lane_out, d_con_len, d_con_status);
@@ -1538,9 +1547,11 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     k_zero<<<g, 256, 0, st>>>(d_cons, d_con_len, d_con_status);
     BB_LAUNCH_CHECK();
   }
+  T.mark("deflate.emit");
   k_emit<<<blk_total, EM_THREADS, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_info, d_plan, d_codes, d_hdr,
                                            d_syms, d_lane_out);
   BB_LAUNCH_CHECK();
+  T.mark("deflate.adler_finalize");
   if (!ad_work.empty()) {
     k_adler_chunks<<<(unsigned)ad_work.size(), AD_THREADS, 0, st>>>(d_lanes, d_ad, d_adl);
     BB_LAUNCH_CHECK();
@@ -1553,6 +1564,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(e->h_pinned) + 8ull * nc, d_con_status, 4ull * nc,
                               cudaMemcpyDeviceToHost, st));
   BB_CUDA_TRY(cudaStreamSynchronize(st));
+  T.finish();
   const int* hs = reinterpret_cast<const int*>(reinterpret_cast<char*>(e->h_pinned) + 8ull * nc);
   for (int c = 0; c < nc; c++) {
     container_len[c] = e->h_pinned[c];

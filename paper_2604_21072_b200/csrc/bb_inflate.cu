@@ -379,11 +379,14 @@ int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStr
     BB_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&e->h_status), sizeof(int) * nj, cudaHostAllocDefault));
     e->h_cap = nj;
   }
+  StageTimer T(st);
+  T.mark("inflate.seq");
   BB_CUDA_TRY(cudaMemcpyAsync(d_jobs, h.data(), sizeof(Job) * nj, cudaMemcpyHostToDevice, st));
   k_inflate_seq<<<nj, 256, 0, st>>>(d_jobs, d_status);
   BB_LAUNCH_CHECK();
   BB_CUDA_TRY(cudaMemcpyAsync(e->h_status, d_status, sizeof(int) * nj, cudaMemcpyDeviceToHost, st));
   BB_CUDA_TRY(cudaStreamSynchronize(st));
+  T.finish();
   for (int i = 0; i < nj; i++) status[i] = e->h_status[i];
   return BB_OK;
 }
