@@ -11,6 +11,7 @@
 // walks the bit stream with shared-memory Huffman tables, then the whole CTA
 // verifies the Adler-32).  It defines correctness and error parity for every
 // input.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -355,17 +356,70 @@ struct InflateEngine {
   Workspace ws;
   int* h_status = nullptr;
   size_t h_cap = 0;
+  ParInflate* par = nullptr;
 };
 
-InflateEngine* inflate_engine_create() { return new InflateEngine(); }
+InflateEngine* inflate_engine_create() {
+  InflateEngine* e = new InflateEngine();
+  e->par = par_inflate_create();
+  return e;
+}
 
 void inflate_engine_destroy(InflateEngine* e) {
   if (!e) return;
   if (e->h_status) cudaFreeHost(e->h_status);
+  par_inflate_destroy(e->par);
   delete e;
 }
 
+static int inflate_seq(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStream_t st, int* status);
+
+static std::atomic<uint64_t> g_par_ok{0}, g_par_fallback{0}, g_seq{0};
+
+// Streams of >= 64 KiB go through the parallel decoder first; whatever it cannot
+// fully validate (and every small stream) is decoded by the exact sequential
+// decoder, which defines the status.
 int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStream_t st, int* status) {
+  const uint64_t kParMin = 1u << 16;
+  std::vector<InflateJob> big, rest;
+  std::vector<int> big_idx, rest_idx;
+  const char* force = getenv("BB_INFLATE_SEQ");
+  for (size_t i = 0; i < jobs.size(); i++) {
+    const InflateJob& j = jobs[i];
+    if (!force && j.n >= kParMin && j.expected > 0 && j.expected < (1ull << 31)) {
+      big.push_back(j);
+      big_idx.push_back((int)i);
+    } else {
+      rest.push_back(j);
+      rest_idx.push_back((int)i);
+    }
+  }
+  if (!big.empty()) {
+    std::vector<int> ok(big.size());
+    int rc = par_inflate(e->par, big, st, ok.data());
+    if (rc) return rc;
+    for (size_t k = 0; k < big.size(); k++) {
+      if (ok[k]) {
+        status[big_idx[k]] = BB_OK;
+        g_par_ok++;
+      } else {
+        g_par_fallback++;
+        rest.push_back(big[k]);
+        rest_idx.push_back(big_idx[k]);
+      }
+    }
+  }
+  if (!rest.empty()) {
+    g_seq += rest.size();
+    std::vector<int> rs(rest.size());
+    int rc = inflate_seq(e, rest, st, rs.data());
+    if (rc) return rc;
+    for (size_t k = 0; k < rest.size(); k++) status[rest_idx[k]] = rs[k];
+  }
+  return BB_OK;
+}
+
+static int inflate_seq(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStream_t st, int* status) {
   const int nj = (int)jobs.size();
   if (nj == 0) return BB_OK;
   int rc = e->ws.reserve(sizeof(Job) * nj + sizeof(int) * nj + 1024);
@@ -392,3 +446,10 @@ int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStr
 }
 
 }  // namespace bb
+
+// Test hook: {parallel-path successes, parallel-path fallbacks, sequential decodes}
+extern "C" BB_API void bb_debug_inflate_counts(uint64_t* out3) {
+  out3[0] = bb::g_par_ok.load();
+  out3[1] = bb::g_par_fallback.load();
+  out3[2] = bb::g_seq.load();
+}

@@ -1,0 +1,1175 @@
+// Parallel inflate of whole zlib streams (the fast path of the deflate backend's
+// decode; the exact sequential decoder in bb_inflate.cu is the fallback that
+// defines uncompress() error parity -- any stream this path cannot fully
+// validate is re-decoded there).
+//
+// A 30+ MiB lane holds thousands of deflate blocks whose boundaries are only
+// known after Huffman-decoding their predecessors.  Instead of walking them in
+// order, every place a block could start is found and decoded at once:
+//
+//   P1 k_candidates   every bit offset is tested for a dynamic-block header
+//                     (BTYPE=10, HLIT<=29, HDIST<=29, complete code-length code);
+//                     every byte offset for a stored block (LEN == ~NLEN);
+//                     results are bitmaps, so ranks give ordered node ids
+//   P2 k_decode_nodes one thread per candidate: full header validation + symbol
+//                     decode to end-of-block (plus any static blocks that follow),
+//                     recording end bit, output bytes and match count
+//   P3 k_link         each node's successor = the candidate that starts exactly
+//                     where it ends (or END / BREAK / BAD)
+//   P4 binary lifting the true block chain is the path from the zlib header;
+//                     jump tables give the i-th block of the chain in O(log)
+//   P5 k_emit_nodes   second decode of the chain's blocks at their final output
+//                     offsets: literals written, matches recorded as (dst,dist,len);
+//                     stored blocks copied by whole CTAs; a BREAK (static block)
+//                     is finished by one thread (k_tail)
+//   P6 LZ77 resolution per 32 KiB output window: pointer jumping in shared
+//                     memory resolves every match byte whose source chain stays in
+//                     the window; the rest are resolved window by window in order
+//                     (k_resolve_ext: one gather per window)
+//   P7 Adler-32 check, size check
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "bb_common.cuh"
+#include "bb_kernels.h"
+
+namespace bb {
+namespace par {
+
+constexpr uint32_t SENT_END = 0xFFFFFFF0u, SENT_BREAK = 0xFFFFFFF1u, SENT_BAD = 0xFFFFFFF2u;
+constexpr int ND_THREADS = 128;
+constexpr uint32_t SUB = 32768;  // resolution window
+constexpr uint32_t MOD = 65521;
+
+__constant__ uint16_t p_lbase[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
+                                     31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t p_lext[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t p_dbase[30] = {1,    2,    3,    4,    5,    7,    9,    13,    17,    25,
+                                     33,   49,   65,   97,   129,  193,  257,  385,   513,   769,
+                                     1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ uint8_t p_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+__constant__ uint8_t p_order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+
+struct PJob {
+  const uint8_t* src;
+  uint64_t n;
+  uint8_t* dst;
+  uint64_t expected;
+  uint64_t dbm;     // dynamic-candidate bitmap: first u32 word (1 bit per stream bit)
+  uint64_t sbm;     // stored-candidate bitmap: first u32 word (1 bit per stream byte)
+  uint32_t node0;   // virtual start node; then ndyn dynamic nodes, then 2*nsto stored nodes
+  uint32_t ndyn, nsto;
+  uint64_t mbase;   // match list base
+  uint64_t mcap;
+  uint32_t sub0, nsub;  // resolution windows
+};
+
+struct Node {
+  uint64_t end_bit;
+  uint64_t out_len;
+  uint32_t nmatch;
+  uint32_t flags;  // bit0 ok, bit1 final, bit2 stored
+  uint64_t start;  // dynamic: header bit; stored: data byte offset (LEN field)
+};
+
+struct Match {
+  uint32_t dst;
+  uint16_t dist;
+  uint16_t len;
+};
+
+// ---- bit access -------------------------------------------------------------
+__device__ __forceinline__ uint64_t load_le64(const uint8_t* p, uint64_t n, uint64_t byte) {
+  uint64_t v = 0;
+  if (byte + 8 <= n) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) v |= (uint64_t)__ldg(p + byte + i) << (8 * i);
+  } else {
+    for (int i = 0; i < 8; i++)
+      if (byte + i < n) v |= (uint64_t)__ldg(p + byte + i) << (8 * i);
+  }
+  return v;
+}
+
+// 64 bits starting at bit `b` (zero beyond the end)
+__device__ __forceinline__ uint64_t peek64(const uint8_t* p, uint64_t n, uint64_t b) {
+  uint64_t byte = b >> 3;
+  uint32_t sh = (uint32_t)(b & 7);
+  uint64_t lo = load_le64(p, n, byte);
+  if (!sh) return lo;
+  uint64_t hi = byte + 8 < n ? __ldg(p + byte + 8) : 0;
+  return (lo >> sh) | (hi << (64 - sh));
+}
+
+struct BitReader {
+  const uint8_t* p;
+  uint64_t n;
+  uint64_t pos;  // next bit to consume (absolute)
+  uint64_t hold;
+  uint32_t bits;
+  __device__ __forceinline__ void init(const uint8_t* p_, uint64_t n_, uint64_t bit) {
+    p = p_;
+    n = n_;
+    pos = bit;
+    hold = peek64(p, n, pos);
+    bits = 64;
+  }
+  __device__ __forceinline__ void refill() {
+    if (bits < 32) {
+      hold = peek64(p, n, pos);
+      bits = 64;
+    }
+  }
+  __device__ __forceinline__ uint32_t peek(uint32_t k) const { return (uint32_t)(hold & ((1ull << k) - 1)); }
+  __device__ __forceinline__ void drop(uint32_t k) {
+    hold >>= k;
+    bits -= k;
+    pos += k;
+  }
+  __device__ __forceinline__ uint32_t take(uint32_t k) {
+    refill();
+    uint32_t v = peek(k);
+    drop(k);
+    return v;
+  }
+  __device__ __forceinline__ bool past_end() const { return pos > 8 * n; }
+};
+
+// ---- canonical decoding tables (limit compare; left-justified 15-bit codes) ----
+template <int CAP>
+struct HTabT {
+  uint16_t lim[16];     // lim[l] for l = 1..15 (lim[0] unused), 15-bit left-justified
+  int16_t base[16];     // sym index = base[l] + (w >> (15 - l))
+  uint16_t sym[CAP];
+  int max;
+};
+typedef HTabT<288> HLit;
+typedef HTabT<32> HDist;
+
+// inftrees.c rules: over-subscribed -> error; incomplete -> error unless
+// (type != CODES and max length == 1).  type: 0 CODES, 1 LENS, 2 DISTS
+template <int CAP>
+__device__ int htab_build(HTabT<CAP>* t, const uint8_t* lens, int n, int type) {
+  uint16_t count[16];
+  for (int i = 0; i < 16; i++) count[i] = 0;
+  for (int s = 0; s < n; s++) count[lens[s]]++;
+  int max = 15;
+  while (max >= 1 && count[max] == 0) max--;
+  t->max = max;
+  if (max == 0) {
+    for (int l = 1; l < 16; l++) t->lim[l] = 0;
+    t->lim[0] = 0;
+    return 0;
+  }
+  int left = 1;
+  for (int len = 1; len <= 15; len++) {
+    left <<= 1;
+    left -= count[len];
+    if (left < 0) return -1;
+  }
+  if (left > 0 && (type == 0 || max != 1)) return -1;
+  uint16_t offs[16];
+  offs[1] = 0;
+  for (int l = 1; l < 15; l++) offs[l + 1] = offs[l] + count[l];
+  uint32_t code = 0;
+  count[0] = 0;
+  for (int l = 1; l <= 15; l++) {
+    code = (code + count[l - 1]) << 1;
+    t->lim[l] = (uint16_t)min((code + count[l]) << (15 - l), 32768u);
+    t->base[l] = (int16_t)((int)offs[l] - (int)code);
+  }
+  for (int s = 0; s < n; s++)
+    if (lens[s]) t->sym[offs[lens[s]]++] = (uint16_t)s;
+  return 0;
+}
+
+// limits held in registers while a block is decoded
+struct Lims {
+  uint32_t v[16];
+  template <int CAP>
+  __device__ __forceinline__ void load(const HTabT<CAP>* t) {
+#pragma unroll
+    for (int k = 1; k < 16; k++) v[k] = t->lim[k];
+  }
+};
+
+// -1 invalid code, -2 past end
+template <int CAP>
+__device__ __forceinline__ int hdecode(BitReader& r, const HTabT<CAP>* t, const Lims& L) {
+  r.refill();
+  uint32_t w = __brev((uint32_t)r.hold) >> 17;
+  int l = 1;
+#pragma unroll
+  for (int k = 1; k < 16; k++) l += (w >= L.v[k]);
+  if (l > 15) return -1;
+  int s = t->sym[t->base[l] + (int)(w >> (15 - l))];
+  r.drop((uint32_t)l);
+  if (r.past_end()) return -2;
+  return s;
+}
+
+template <int CAP>
+__device__ __forceinline__ int hdecode(BitReader& r, const HTabT<CAP>* t) {
+  Lims L;
+  L.load(t);
+  return hdecode(r, t, L);
+}
+
+struct Tables {
+  HLit lit;
+  HDist dist;
+};
+
+__device__ void static_tables(Tables* T) {
+  uint8_t lens[288];
+  for (int i = 0; i < 288; i++) lens[i] = i < 144 ? 8 : i < 256 ? 9 : i < 280 ? 7 : 8;
+  htab_build(&T->lit, lens, 288, 1);
+  for (int i = 0; i < 30; i++) lens[i] = 5;
+  lens[30] = lens[31] = 5;
+  htab_build(&T->dist, lens, 32, 2);
+}
+
+// Reads a dynamic block header at r (positioned after the 3 header bits).
+__device__ int read_dynamic(BitReader& r, Tables* T) {
+  uint32_t nlen = r.take(5) + 257, ndist = r.take(5) + 1, ncode = r.take(4) + 4;
+  if (nlen > 286 || ndist > 30) return -1;
+  uint8_t lens[320];
+  for (int i = 0; i < 19; i++) lens[i] = 0;
+  for (uint32_t i = 0; i < ncode; i++) lens[p_order[i]] = (uint8_t)r.take(3);
+  if (r.past_end()) return -1;
+  HDist* ch = &T->dist;  // scratch for the code-length code
+  if (htab_build(ch, lens, 19, 0)) return -1;
+  uint32_t have = 0;
+  while (have < nlen + ndist) {
+    int sym;
+    if (ch->max == 0) {
+      r.take(1);
+      sym = 0;
+    } else {
+      sym = hdecode(r, ch);
+      if (sym < 0) return -1;
+    }
+    if (sym < 16) {
+      lens[have++] = (uint8_t)sym;
+    } else {
+      uint32_t len = 0, copy;
+      if (sym == 16) {
+        if (have == 0) return -1;
+        len = lens[have - 1];
+        copy = 3 + r.take(2);
+      } else if (sym == 17) {
+        copy = 3 + r.take(3);
+      } else {
+        copy = 11 + r.take(7);
+      }
+      if (have + copy > nlen + ndist) return -1;
+      while (copy--) lens[have++] = (uint8_t)len;
+    }
+    if (r.past_end()) return -1;
+  }
+  if (lens[256] == 0) return -1;
+  if (htab_build(&T->lit, lens, nlen, 1)) return -1;
+  if (htab_build(&T->dist, lens + nlen, ndist, 2)) return -1;
+  return 0;
+}
+
+// Decodes symbols until END_BLOCK.  EMIT: writes literals to out[] and match
+// records; otherwise only counts.  Returns 0 ok, -1 error.
+template <bool EMIT>
+__device__ int decode_codes(BitReader& r, const Tables* T, uint64_t& out_len, uint32_t& nmatch, uint64_t limit,
+                            uint8_t* out, uint64_t out_off, Match* matches, uint64_t mcap) {
+  Lims LL, DL;
+  LL.load(&T->lit);
+  DL.load(&T->dist);
+  for (;;) {
+    int sym = hdecode(r, &T->lit, LL);
+    if (sym < 0) return -1;
+    if (sym < 256) {
+      if (out_len >= limit) return -1;
+      if (EMIT) out[out_off + out_len] = (uint8_t)sym;
+      out_len++;
+    } else if (sym == 256) {
+      return 0;
+    } else {
+      sym -= 257;
+      if (sym >= 29) return -1;
+      uint32_t len = p_lbase[sym] + r.take(p_lext[sym]);
+      int ds = hdecode(r, &T->dist, DL);
+      if (ds < 0 || ds >= 30) return -1;
+      uint32_t dist = p_dbase[ds] + r.take(p_dext[ds]);
+      if (r.past_end()) return -1;
+      if (out_len + len > limit) return -1;
+      if (EMIT) {
+        if (dist > out_off + out_len) return -1;  // invalid distance too far back
+        if (nmatch >= mcap) return -1;
+        matches[nmatch] = Match{(uint32_t)(out_off + out_len), (uint16_t)dist, (uint16_t)len};
+      }
+      nmatch++;
+      out_len += len;
+    }
+  }
+}
+
+// ---- P1 --------------------------------------------------------------------
+__device__ __forceinline__ uint32_t bits_at(uint64_t w0, uint64_t w1, uint32_t off, uint32_t k) {
+  uint64_t v = off < 64 ? (w0 >> off) | (off ? (w1 << (64 - off)) : 0) : (w1 >> (off - 64));
+  return (uint32_t)(v & ((1ull << k) - 1));
+}
+
+__device__ __forceinline__ bool dyn_header_ok(const uint8_t* p, uint64_t n, uint64_t b) {
+  if (b + 17 > 8 * n) return false;
+  uint64_t w0 = peek64(p, n, b);
+  if (((w0 >> 1) & 3) != 2) return false;
+  if (((w0 >> 3) & 31) > 29 || ((w0 >> 8) & 31) > 29) return false;
+  uint32_t ncode = (uint32_t)((w0 >> 13) & 15) + 4;
+  uint64_t w1 = peek64(p, n, b + 64);
+  uint32_t kraft = 0;
+  for (uint32_t i = 0; i < ncode; i++) {
+    uint32_t l = bits_at(w0, w1, 17 + 3 * i, 3);
+    if (l) kraft += 128u >> l;
+  }
+  return kraft == 128;
+}
+
+__global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __restrict__ job_of_block,
+                             const uint64_t* __restrict__ block_byte0, uint32_t* __restrict__ dbm,
+                             uint32_t* __restrict__ sbm) {
+  const uint32_t j = job_of_block[blockIdx.x];
+  const PJob J = jobs[j];
+  const uint64_t B = block_byte0[blockIdx.x] + threadIdx.x;  // one stream byte per thread
+  const int lane = threadIdx.x & 31;
+  uint32_t dbits = 0;
+  bool st = false;
+  if (B < J.n) {
+    for (int k = 0; k < 8; k++) {
+      uint64_t b = 8 * B + k;
+      if (b >= 16 && dyn_header_ok(J.src, J.n, b)) dbits |= 1u << k;
+    }
+    if (B >= 2 && B + 4 <= J.n) {
+      uint32_t len = __ldg(J.src + B) | ((uint32_t)__ldg(J.src + B + 1) << 8);
+      uint32_t nlen = __ldg(J.src + B + 2) | ((uint32_t)__ldg(J.src + B + 3) << 8);
+      st = len == (~nlen & 0xffff) && B + 4 + len <= J.n;
+    }
+  }
+  // dynamic bitmap: byte B of the stream -> byte B of the bitmap
+  if (B < J.n) reinterpret_cast<uint8_t*>(dbm + J.dbm)[B] = (uint8_t)dbits;
+  unsigned ball = __ballot_sync(0xffffffffu, st);
+  if (lane == 0 && B < J.n + 32) sbm[J.sbm + (B >> 5)] = ball;
+}
+
+__global__ void k_popc(const uint32_t* __restrict__ words, uint64_t count, uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = __popc(words[i]);
+}
+
+// ---- P2 --------------------------------------------------------------------
+// rank of the set bit `bit` within job-local bitmap words [w0, ...) via per-word prefix counts
+__device__ __forceinline__ uint32_t bm_rank(const uint32_t* words, const uint32_t* prefix, uint64_t w0, uint64_t bit) {
+  uint64_t w = w0 + (bit >> 5);
+  return prefix[w] - prefix[w0] + __popc(words[w] & ((1u << (bit & 31)) - 1));
+}
+__device__ __forceinline__ bool bm_test(const uint32_t* words, uint64_t w0, uint64_t bit) {
+  return (words[w0 + (bit >> 5)] >> (bit & 31)) & 1;
+}
+
+// fill node positions: thread per bitmap word
+__global__ void k_node_positions(const PJob* __restrict__ jobs, int njobs, const uint32_t* __restrict__ dbm,
+                                 const uint32_t* __restrict__ dpre, const uint32_t* __restrict__ sbm,
+                                 const uint32_t* __restrict__ spre, Node* __restrict__ nodes) {
+  const int j = blockIdx.y;
+  const PJob J = jobs[j];
+  const uint64_t dwords = (J.n + 3) / 4, swords = (J.n + 31) / 32 + 1;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < dwords + swords;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    if (w < dwords) {
+      uint32_t v = dbm[J.dbm + w];
+      uint32_t r = dpre[J.dbm + w] - dpre[J.dbm];
+      while (v) {
+        int k = __ffs(v) - 1;
+        v &= v - 1;
+        Node nd{};
+        nd.start = 32 * w + k;
+        nodes[J.node0 + 1 + r++] = nd;
+      }
+    } else {
+      uint64_t ws = w - dwords;
+      uint32_t v = sbm[J.sbm + ws];
+      uint32_t r = spre[J.sbm + ws] - spre[J.sbm];
+      while (v) {
+        int k = __ffs(v) - 1;
+        v &= v - 1;
+        uint64_t B = 32 * ws + k;
+        for (int f = 0; f < 2; f++) {
+          Node nd{};
+          nd.start = B;
+          nd.flags = 4 | (f ? 2 : 0);
+          nodes[J.node0 + 1 + J.ndyn + 2 * r + f] = nd;
+        }
+        r++;
+      }
+    }
+  }
+}
+
+__device__ int decode_static_run(BitReader& r, Tables* T, uint64_t& out_len, uint32_t& nmatch, uint64_t limit,
+                                 bool& final_seen) {
+  // continue through static blocks that directly follow (counting only)
+  for (;;) {
+    r.refill();
+    uint32_t hdr = r.peek(3);
+    if (((hdr >> 1) & 3) != 1) return 0;  // not static: node ends here
+    r.drop(3);
+    static_tables(T);
+    if (decode_codes<false>(r, T, out_len, nmatch, limit, nullptr, 0, nullptr, 0)) return -1;
+    if (hdr & 1) {
+      final_seen = true;
+      return 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(ND_THREADS) k_decode_nodes(const PJob* __restrict__ jobs,
+                                                             const uint32_t* __restrict__ node_job,
+                                                             uint32_t nnodes, Node* __restrict__ nodes) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  Tables* T = reinterpret_cast<Tables*>(sm) + threadIdx.x;
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nnodes) return;
+  const PJob J = jobs[node_job[g]];
+  Node nd = nodes[g];
+  if (g == J.node0) {  // virtual start: "a block ended at bit 16"
+    nd.end_bit = 16;
+    nd.out_len = 0;
+    nd.nmatch = 0;
+    nd.flags = 1;
+    nodes[g] = nd;
+    return;
+  }
+  if (nd.flags & 4) {  // stored
+    uint64_t B = nd.start;
+    uint32_t len = J.src[B] | ((uint32_t)J.src[B + 1] << 8);
+    nd.end_bit = 8 * (B + 4 + len);
+    nd.out_len = len;
+    nd.nmatch = 0;
+    nd.flags |= (len <= J.expected) ? 1 : 0;
+    nodes[g] = nd;
+    return;
+  }
+  BitReader r;
+  r.init(J.src, J.n, nd.start);
+  uint32_t hdr = r.take(3);
+  bool final_seen = hdr & 1;
+  uint64_t out_len = 0;
+  uint32_t nmatch = 0;
+  int rc = read_dynamic(r, T);
+  if (!rc) rc = decode_codes<false>(r, T, out_len, nmatch, J.expected, nullptr, 0, nullptr, 0);
+  if (!rc && !final_seen) rc = decode_static_run(r, T, out_len, nmatch, J.expected, final_seen);
+  nd.end_bit = r.pos;
+  nd.out_len = out_len;
+  nd.nmatch = nmatch;
+  nd.flags = (rc == 0 ? 1 : 0) | (final_seen ? 2 : 0);
+  nodes[g] = nd;
+}
+
+// ---- P3 --------------------------------------------------------------------
+__global__ void k_link(const PJob* __restrict__ jobs, const uint32_t* __restrict__ node_job, uint32_t nnodes,
+                       const Node* __restrict__ nodes, const uint32_t* __restrict__ dbm,
+                       const uint32_t* __restrict__ dpre, const uint32_t* __restrict__ sbm,
+                       const uint32_t* __restrict__ spre, uint32_t* __restrict__ next) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nnodes) return;
+  const PJob J = jobs[node_job[g]];
+  const Node nd = nodes[g];
+  uint32_t nx;
+  if (!(nd.flags & 1)) {
+    nx = SENT_BAD;
+  } else if (nd.flags & 2) {
+    nx = SENT_END;
+  } else {
+    uint64_t e = nd.end_bit;
+    if (e + 3 > 8 * J.n) {
+      nx = SENT_BAD;
+    } else {
+      uint32_t h = (uint32_t)(peek64(J.src, J.n, e) & 7);
+      uint32_t type = (h >> 1) & 3;
+      if (type == 2) {
+        nx = bm_test(dbm, J.dbm, e) ? J.node0 + 1 + bm_rank(dbm, dpre, J.dbm, e) : SENT_BAD;
+      } else if (type == 0) {
+        uint64_t B = (e + 3 + 7) >> 3;
+        nx = (B < J.n && bm_test(sbm, J.sbm, B)) ? J.node0 + 1 + J.ndyn + 2 * bm_rank(sbm, spre, J.sbm, B) + (h & 1)
+                                                 : SENT_BAD;
+      } else if (type == 1) {
+        nx = SENT_BREAK;
+      } else {
+        nx = SENT_BAD;
+      }
+    }
+  }
+  next[g] = nx;
+}
+
+// ---- P4 --------------------------------------------------------------------
+__global__ void k_lift(const uint32_t* __restrict__ prev, uint32_t* __restrict__ cur, uint32_t nnodes) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nnodes) return;
+  uint32_t a = prev[g];
+  cur[g] = a >= SENT_END ? a : prev[a];
+}
+
+struct Chain {
+  uint32_t len;       // blocks on the chain (excluding the virtual start)
+  uint32_t terminal;  // SENT_END / SENT_BREAK / SENT_BAD
+  uint32_t last;      // last node (the virtual start if len == 0)
+  uint32_t pad;
+};
+
+__global__ void k_chain_len(const PJob* __restrict__ jobs, int njobs, const uint32_t* __restrict__ jump,
+                            uint32_t nnodes, int levels, Chain* __restrict__ chains) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  uint32_t v = jobs[j].node0, len = 0;
+  for (int k = levels - 1; k >= 0; k--) {
+    uint32_t u = jump[(uint64_t)k * nnodes + v];
+    if (u < SENT_END) {
+      v = u;
+      len += 1u << k;
+    }
+  }
+  chains[j] = Chain{len, jump[v], v, 0};
+}
+
+// chain[j][i] = node at step i+1 from the start
+__global__ void k_chain_nodes(const PJob* __restrict__ jobs, const Chain* __restrict__ chains,
+                              const uint32_t* __restrict__ jump, uint32_t nnodes, int levels,
+                              uint32_t* __restrict__ chain_nodes) {
+  const int j = blockIdx.y;
+  const PJob J = jobs[j];
+  const uint32_t len = chains[j].len;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    uint32_t v = J.node0, steps = i + 1;
+    for (int k = 0; k < levels; k++)
+      if (steps >> k & 1) v = jump[(uint64_t)k * nnodes + v];
+    chain_nodes[J.node0 + i] = v;  // node0-based slots: chain length <= node count
+  }
+}
+
+// exclusive scans of out_len / nmatch along each chain (one CTA per job)
+__global__ void __launch_bounds__(256) k_chain_scan(const PJob* __restrict__ jobs, const Chain* __restrict__ chains,
+                                                   const uint32_t* __restrict__ chain_nodes,
+                                                   const Node* __restrict__ nodes, uint64_t* __restrict__ out_off,
+                                                   uint64_t* __restrict__ m_off, uint64_t* __restrict__ totals) {
+  typedef cub::BlockScan<uint64_t, 256> Scan;
+  __shared__ typename Scan::TempStorage t1, t2;
+  __shared__ uint64_t c_out, c_m;
+  const int j = blockIdx.x;
+  const PJob J = jobs[j];
+  const uint32_t len = chains[j].len;
+  if (threadIdx.x == 0) c_out = c_m = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < len; base += 256) {
+    uint32_t i = base + threadIdx.x;
+    uint64_t o = 0, m = 0;
+    if (i < len) {
+      const Node& nd = nodes[chain_nodes[J.node0 + i]];
+      o = nd.out_len;
+      m = nd.nmatch;
+    }
+    uint64_t xo, xm, ao, am;
+    Scan(t1).ExclusiveSum(o, xo, ao);
+    Scan(t2).ExclusiveSum(m, xm, am);
+    if (i < len) {
+      out_off[J.node0 + i] = c_out + xo;
+      m_off[J.node0 + i] = c_m + xm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c_out += ao;
+      c_m += am;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    totals[2 * j] = c_out;
+    totals[2 * j + 1] = c_m;
+  }
+}
+
+// ---- P5 --------------------------------------------------------------------
+__global__ void __launch_bounds__(ND_THREADS) k_emit_nodes(const PJob* __restrict__ jobs, int njobs,
+                                                           const Chain* __restrict__ chains,
+                                                           const uint32_t* __restrict__ chain_nodes,
+                                                           const uint32_t* __restrict__ job_of_chain_block,
+                                                           const uint32_t* __restrict__ chain_block_base,
+                                                           const Node* __restrict__ nodes,
+                                                           const uint64_t* __restrict__ out_off,
+                                                           const uint64_t* __restrict__ m_off, Match* __restrict__ matches,
+                                                           uint32_t* __restrict__ fail) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  Tables* T = reinterpret_cast<Tables*>(sm) + threadIdx.x;
+  const uint32_t j = job_of_chain_block[blockIdx.x];
+  const PJob J = jobs[j];
+  const uint32_t i = (blockIdx.x - chain_block_base[j]) * blockDim.x + threadIdx.x;
+  if (i >= chains[j].len) return;
+  const Node nd = nodes[chain_nodes[J.node0 + i]];
+  if (nd.flags & 4) return;  // stored: copied by k_copy_stored
+  const uint64_t off = out_off[J.node0 + i];
+  Match* mm = matches + J.mbase + m_off[J.node0 + i];
+  BitReader r;
+  r.init(J.src, J.n, nd.start);
+  uint32_t hdr = r.take(3);
+  bool final_seen = hdr & 1;
+  uint64_t out_len = 0;
+  uint32_t nmatch = 0;
+  const uint64_t limit = nd.out_len;
+  int rc = read_dynamic(r, T);
+  if (!rc) rc = decode_codes<true>(r, T, out_len, nmatch, limit, J.dst, off, mm, nd.nmatch);
+  while (!rc && !final_seen) {
+    r.refill();
+    uint32_t h = r.peek(3);
+    if (((h >> 1) & 3) != 1) break;
+    r.drop(3);
+    static_tables(T);
+    rc = decode_codes<true>(r, T, out_len, nmatch, limit, J.dst, off, mm, nd.nmatch);
+    final_seen = h & 1;
+  }
+  if (rc || out_len != nd.out_len) atomicExch(&fail[j], 1u);
+}
+
+// stored blocks of the chain: one CTA per block, byte-parallel copy
+__global__ void k_copy_stored(const PJob* __restrict__ jobs, const Chain* __restrict__ chains,
+                              const uint32_t* __restrict__ chain_nodes, const Node* __restrict__ nodes,
+                              const uint64_t* __restrict__ out_off, const uint32_t* __restrict__ job_of_block,
+                              const uint32_t* __restrict__ block_base) {
+  const uint32_t j = job_of_block[blockIdx.x];
+  const PJob J = jobs[j];
+  const uint32_t i = blockIdx.x - block_base[j];
+  if (i >= chains[j].len) return;
+  const Node nd = nodes[chain_nodes[J.node0 + i]];
+  if (!(nd.flags & 4)) return;
+  const uint8_t* s = J.src + nd.start + 4;
+  uint8_t* d = J.dst + out_off[J.node0 + i];
+  for (uint64_t k = threadIdx.x; k < nd.out_len; k += blockDim.x) d[k] = s[k];
+}
+
+// Sequential continuation after a BREAK (static block not covered by a node) and
+// the trailer.  One thread per job.
+__global__ void k_tail(const PJob* __restrict__ jobs, int njobs, const Chain* __restrict__ chains,
+                       const Node* __restrict__ nodes, const uint64_t* __restrict__ totals,
+                       Match* __restrict__ matches, uint32_t* __restrict__ fail, uint64_t* __restrict__ out_total,
+                       uint32_t* __restrict__ want_adler, Tables* __restrict__ tabs) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  const PJob J = jobs[j];
+  const Chain C = chains[j];
+  uint64_t out_len = totals[2 * j];
+  uint64_t nm = totals[2 * j + 1];
+  const Node last = nodes[C.last];
+  uint64_t end = last.end_bit;
+  if (C.terminal == SENT_BAD) {
+    fail[j] = 1;
+    return;
+  }
+  if (C.terminal == SENT_BREAK) {
+    Tables* T = tabs + j;
+    BitReader r;
+    r.init(J.src, J.n, end);
+    bool final_seen = false;
+    while (!final_seen) {
+      uint32_t h = r.take(3);
+      if (r.past_end()) {
+        fail[j] = 1;
+        return;
+      }
+      final_seen = h & 1;
+      uint32_t type = (h >> 1) & 3;
+      int rc = 0;
+      uint32_t nmatch = 0;
+      uint64_t before = out_len;
+      if (type == 0) {
+        uint64_t B = (r.pos + 7) >> 3;
+        if (B + 4 > J.n) {
+          fail[j] = 1;
+          return;
+        }
+        uint32_t len = J.src[B] | ((uint32_t)J.src[B + 1] << 8);
+        uint32_t nlen = J.src[B + 2] | ((uint32_t)J.src[B + 3] << 8);
+        if (len != (~nlen & 0xffff) || B + 4 + len > J.n || out_len + len > J.expected) {
+          fail[j] = 1;
+          return;
+        }
+        for (uint32_t k = 0; k < len; k++) J.dst[out_len + k] = J.src[B + 4 + k];
+        out_len += len;
+        r.init(J.src, J.n, 8 * (B + 4 + len));
+        continue;
+      } else if (type == 1) {
+        static_tables(T);
+      } else if (type == 2) {
+        rc = read_dynamic(r, T);
+      } else {
+        rc = -1;
+      }
+      uint64_t added = 0;
+      if (!rc)
+        rc = decode_codes<true>(r, T, added, nmatch, J.expected - before, J.dst, before, matches + J.mbase + nm,
+                                J.mcap - nm);
+      if (rc) {
+        fail[j] = 1;
+        return;
+      }
+      out_len = before + added;
+      nm += nmatch;
+    }
+    end = r.pos;
+  }
+  out_total[2 * j] = out_len;
+  out_total[2 * j + 1] = nm;
+  // trailer: byte-aligned big-endian Adler-32
+  uint64_t tb = (end + 7) >> 3;
+  if (tb + 4 > J.n) {
+    fail[j] = 1;
+    return;
+  }
+  want_adler[j] = ((uint32_t)J.src[tb] << 24) | ((uint32_t)J.src[tb + 1] << 16) | ((uint32_t)J.src[tb + 2] << 8) |
+                  J.src[tb + 3];
+  if (out_len != J.expected) fail[j] = 1;
+}
+
+// ---- P6 --------------------------------------------------------------------
+// lower bound: first match with dst + len > x (matches sorted by dst)
+__device__ uint64_t first_match_after(const Match* m, uint64_t count, uint64_t x) {
+  uint64_t lo = 0, hi = count;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    if ((uint64_t)m[mid].dst + m[mid].len > x) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+constexpr uint32_t RESOLVED = 0x80000000u;
+constexpr int RS_THREADS = 1024;
+
+struct ExtEntry {
+  uint32_t dst;
+  uint32_t src;
+};
+
+__global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __restrict__ jobs,
+                                                              const uint32_t* __restrict__ job_of_sub,
+                                                              const uint64_t* __restrict__ out_total,
+                                                              const uint32_t* __restrict__ fail,
+                                                              const Match* __restrict__ matches,
+                                                              ExtEntry* __restrict__ ext,
+                                                              uint32_t* __restrict__ ext_cnt) {
+  extern __shared__ uint32_t ent[];  // SUB entries: RESOLVED | value, or source relative to S - 65536
+  __shared__ int changed;
+  __shared__ uint32_t s_cnt;
+  const uint32_t j = job_of_sub[blockIdx.x];
+  const PJob J = jobs[j];
+  const uint32_t sub = blockIdx.x - J.sub0;
+  if (fail[j]) return;
+  const uint64_t total = out_total[2 * j];
+  const uint64_t S = (uint64_t)sub * SUB;
+  if (S >= total) return;
+  const uint32_t W = (uint32_t)min((uint64_t)SUB, total - S);
+  const uint64_t nm = out_total[2 * j + 1];
+  const Match* M = matches + J.mbase;
+  for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) ent[i] = RESOLVED | J.dst[S + i];
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  // match bytes -> source pointers
+  const uint64_t m0 = first_match_after(M, nm, S);
+  for (uint64_t k = m0 + threadIdx.x; k < nm && M[k].dst < S + W; k += blockDim.x) {
+    const Match mt = M[k];
+    uint64_t a = max((uint64_t)mt.dst, S), b = min((uint64_t)mt.dst + mt.len, S + W);
+    for (uint64_t x = a; x < b; x++) ent[x - S] = (uint32_t)(x - mt.dist - S + 65536);
+  }
+  __syncthreads();
+  // pointer jumping inside the window
+  do {
+    __syncthreads();
+    if (threadIdx.x == 0) changed = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
+      uint32_t e = ent[i];
+      if (e & RESOLVED) continue;
+      if (e < 65536) continue;  // source before the window: external
+      uint32_t t = ent[e - 65536];
+      ent[i] = t;  // either the resolved value or a pointer closer to the root
+      changed = 1;
+    }
+    __syncthreads();
+  } while (changed);
+  for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
+    uint32_t e = ent[i];
+    if (e & RESOLVED) {
+      J.dst[S + i] = (uint8_t)e;
+    } else {
+      uint32_t k = atomicAdd(&s_cnt, 1u);
+      ext[(uint64_t)blockIdx.x * SUB + k] = ExtEntry{(uint32_t)(S + i), (uint32_t)(S + e - 65536)};
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ext_cnt[blockIdx.x] = s_cnt;
+}
+
+__global__ void __launch_bounds__(1024) k_resolve_ext(const PJob* __restrict__ jobs,
+                                                      const uint64_t* __restrict__ out_total,
+                                                      const uint32_t* __restrict__ fail,
+                                                      const ExtEntry* __restrict__ ext,
+                                                      const uint32_t* __restrict__ ext_cnt) {
+  const PJob J = jobs[blockIdx.x];
+  if (fail[blockIdx.x]) return;
+  const uint64_t total = out_total[2 * blockIdx.x];
+  const uint32_t nsub = (uint32_t)((total + SUB - 1) / SUB);
+  for (uint32_t s = 0; s < nsub; s++) {
+    const uint32_t g = J.sub0 + s;
+    const uint32_t c = ext_cnt[g];
+    const ExtEntry* E = ext + (uint64_t)g * SUB;
+    for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
+      ExtEntry e = E[k];
+      J.dst[e.dst] = J.dst[e.src];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- P7 Adler ---------------------------------------------------------------
+constexpr int PA_THREADS = 256;
+constexpr uint64_t PA_CHUNK = 64 * 1024;
+
+__global__ void __launch_bounds__(PA_THREADS) k_adler_part(const PJob* __restrict__ jobs,
+                                                          const uint32_t* __restrict__ job_of_chunk,
+                                                          const uint32_t* __restrict__ chunk_base,
+                                                          uint4* __restrict__ part) {
+  __shared__ uint32_t wa[PA_THREADS / 32], wb[PA_THREADS / 32];
+  __shared__ uint64_t wm[PA_THREADS / 32];
+  const uint32_t j = job_of_chunk[blockIdx.x];
+  const PJob J = jobs[j];
+  const uint64_t c = blockIdx.x - chunk_base[j];
+  const uint64_t per = PA_CHUNK / PA_THREADS;
+  const uint64_t c0 = min(c * PA_CHUNK + threadIdx.x * per, J.expected);
+  const uint64_t c1 = min(c0 + per, min((c + 1) * PA_CHUNK, J.expected));
+  uint64_t A = 0, B = 0;
+  for (uint64_t i = c0; i < c1; i++) {
+    A += J.dst[i];
+    B += A;
+  }
+  A %= MOD;
+  B %= MOD;
+  uint64_t m = c1 - c0;
+  for (int off = 1; off < 32; off <<= 1) {
+    uint64_t rA = __shfl_down_sync(0xffffffffu, A, off);
+    uint64_t rB = __shfl_down_sync(0xffffffffu, B, off);
+    uint64_t rm = __shfl_down_sync(0xffffffffu, m, off);
+    int lane = threadIdx.x & 31;
+    if (lane + off < 32 && (lane & (2 * off - 1)) == 0) {
+      B = (B + rB + (rm % MOD) * A) % MOD;
+      A = (A + rA) % MOD;
+      m += rm;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    wa[threadIdx.x >> 5] = (uint32_t)A;
+    wb[threadIdx.x >> 5] = (uint32_t)B;
+    wm[threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t TA = 0, TB = 0, TM = 0;
+    for (int w = 0; w < PA_THREADS / 32; w++) {
+      TB = (TB + wb[w] + (wm[w] % MOD) * TA) % MOD;
+      TA = (TA + wa[w]) % MOD;
+      TM += wm[w];
+    }
+    part[blockIdx.x] = make_uint4((uint32_t)TA, (uint32_t)TB, (uint32_t)TM, (uint32_t)(TM >> 32));
+  }
+}
+
+__global__ void k_adler_check(const PJob* __restrict__ jobs, int njobs, const uint32_t* __restrict__ chunk_base,
+                              const uint4* __restrict__ part, const uint32_t* __restrict__ want,
+                              uint32_t* __restrict__ fail) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs || fail[j]) return;
+  const PJob J = jobs[j];
+  uint64_t nch = (J.expected + PA_CHUNK - 1) / PA_CHUNK;
+  uint64_t TA = 0, TB = 0;
+  for (uint64_t c = 0; c < nch; c++) {
+    uint4 p = part[chunk_base[j] + c];
+    uint64_t m = p.z | ((uint64_t)p.w << 32);
+    TB = (TB + p.y + (m % MOD) * TA) % MOD;
+    TA = (TA + p.x) % MOD;
+  }
+  uint32_t a = (uint32_t)((1 + TA) % MOD), b = (uint32_t)((J.expected % MOD + TB) % MOD);
+  if (((b << 16) | a) != want[j]) fail[j] = 1;
+}
+
+}  // namespace par
+
+// ---------------------------------------------------------------------------
+// host orchestration
+
+struct ParInflate {
+  Workspace ws, nodesw, lists;
+  uint32_t* h_pin = nullptr;
+  size_t h_cap = 0;
+  void* scan_tmp = nullptr;
+  size_t scan_cap = 0;
+  ~ParInflate() {
+    if (h_pin) cudaFreeHost(h_pin);
+    if (scan_tmp) cudaFree(scan_tmp);
+  }
+};
+
+ParInflate* par_inflate_create() { return new ParInflate(); }
+void par_inflate_destroy(ParInflate* p) { delete p; }
+
+int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t st, int* ok) {
+  using namespace par;
+  const int nj = (int)jobs.size();
+  if (!nj) return BB_OK;
+  StageTimer T(st);
+  T.mark("inflate.candidates");
+  static bool attr = false;
+  size_t nd_smem = sizeof(Tables) * ND_THREADS;
+  if (!attr) {
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_emit_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
+    attr = true;
+  }
+  std::vector<PJob> J(nj);
+  std::vector<uint32_t> cand_job, sub_job, chunk_job, chunk_base(nj);
+  std::vector<uint64_t> cand_byte0;
+  uint64_t dwords = 0, swords = 0, mtot = 0;
+  uint32_t subs = 0;
+  for (int i = 0; i < nj; i++) {
+    PJob& p = J[i];
+    p = PJob{};
+    p.src = jobs[i].src;
+    p.n = jobs[i].n;
+    p.dst = jobs[i].dst;
+    p.expected = jobs[i].expected;
+    p.dbm = dwords;
+    p.sbm = swords;
+    dwords += (p.n + 3) / 4 + 1;
+    swords += (p.n + 31) / 32 + 2;
+    p.mbase = mtot;
+    p.mcap = p.expected / 3 + 1;
+    mtot += p.mcap;
+    p.sub0 = subs;
+    p.nsub = (uint32_t)((p.expected + SUB - 1) / SUB);
+    subs += p.nsub;
+    for (uint32_t s = 0; s < p.nsub; s++) sub_job.push_back(i);
+    for (uint64_t b = 0; b < p.n; b += 256) {
+      cand_job.push_back(i);
+      cand_byte0.push_back(b);
+    }
+    chunk_base[i] = (uint32_t)chunk_job.size();
+    for (uint64_t c = 0; c * PA_CHUNK < p.expected; c++) chunk_job.push_back(i);
+  }
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t need = al(sizeof(PJob) * nj) + al(4 * cand_job.size()) + al(8 * cand_byte0.size()) + 2 * al(4 * dwords) +
+                2 * al(4 * swords) + al(4 * sub_job.size() + 4) + al(4 * chunk_job.size() + 4) + al(4 * nj) +
+                al(16 * chunk_job.size() + 16) + al(sizeof(Match) * mtot) + al(sizeof(ExtEntry) * (uint64_t)subs * SUB) +
+                al(4 * subs + 4) + al(4 * nj) * 6 + al(16 * nj) * 4 + al(sizeof(Chain) * nj) +
+                al(sizeof(Tables) * nj) + 65536;
+  int rc = P->ws.reserve(need);
+  if (rc) return rc;
+  Workspace& W = P->ws;
+  PJob* d_jobs = W.take<PJob>(nj);
+  uint32_t* d_cand_job = W.take<uint32_t>(cand_job.size());
+  uint64_t* d_cand_byte0 = W.take<uint64_t>(cand_byte0.size());
+  uint32_t* d_dbm = W.take<uint32_t>(dwords);
+  uint32_t* d_dpre = W.take<uint32_t>(dwords);
+  uint32_t* d_sbm = W.take<uint32_t>(swords);
+  uint32_t* d_spre = W.take<uint32_t>(swords);
+  uint32_t* d_sub_job = W.take<uint32_t>(sub_job.size() + 1);
+  uint32_t* d_chunk_job = W.take<uint32_t>(chunk_job.size() + 1);
+  uint32_t* d_chunk_base = W.take<uint32_t>(nj);
+  uint4* d_part = W.take<uint4>(chunk_job.size() + 1);
+  Match* d_matches = W.take<Match>(mtot);
+  ExtEntry* d_ext = W.take<ExtEntry>((uint64_t)subs * SUB);
+  uint32_t* d_ext_cnt = W.take<uint32_t>(subs + 1);
+  uint32_t* d_fail = W.take<uint32_t>(nj);
+  uint32_t* d_want = W.take<uint32_t>(nj);
+  uint64_t* d_totals = W.take<uint64_t>(2 * nj);
+  uint64_t* d_out_total = W.take<uint64_t>(2 * nj);
+  Chain* d_chains = W.take<Chain>(nj);
+  Tables* d_tabs = W.take<Tables>(nj);
+
+  BB_CUDA_TRY(cudaMemcpyAsync(d_jobs, J.data(), sizeof(PJob) * nj, cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_cand_job, cand_job.data(), 4 * cand_job.size(), cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_cand_byte0, cand_byte0.data(), 8 * cand_byte0.size(), cudaMemcpyHostToDevice, st));
+  if (!sub_job.empty())
+    BB_CUDA_TRY(cudaMemcpyAsync(d_sub_job, sub_job.data(), 4 * sub_job.size(), cudaMemcpyHostToDevice, st));
+  if (!chunk_job.empty())
+    BB_CUDA_TRY(cudaMemcpyAsync(d_chunk_job, chunk_job.data(), 4 * chunk_job.size(), cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_chunk_base, chunk_base.data(), 4 * nj, cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemsetAsync(d_dbm, 0, 4 * dwords, st));
+  BB_CUDA_TRY(cudaMemsetAsync(d_sbm, 0, 4 * swords, st));
+  BB_CUDA_TRY(cudaMemsetAsync(d_fail, 0, 4 * nj, st));
+
+  // P1
+  k_candidates<<<(unsigned)cand_job.size(), 256, 0, st>>>(d_jobs, d_cand_job, d_cand_byte0, d_dbm, d_sbm);
+  BB_LAUNCH_CHECK();
+  k_popc<<<grid_for(dwords, 256, 8), 256, 0, st>>>(d_dbm, dwords, d_dpre);
+  BB_LAUNCH_CHECK();
+  k_popc<<<grid_for(swords, 256, 8), 256, 0, st>>>(d_sbm, swords, d_spre);
+  BB_LAUNCH_CHECK();
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_dpre, d_dpre, (int)dwords, st);
+  size_t tmp2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, d_spre, d_spre, (int)swords, st);
+  tmp = std::max(tmp, tmp2);
+  if (tmp > P->scan_cap) {
+    if (P->scan_tmp) cudaFree(P->scan_tmp);
+    BB_CUDA_TRY(cudaMalloc(&P->scan_tmp, tmp));
+    P->scan_cap = tmp;
+  }
+  // exclusive scan in place (CUB supports aliasing for ExclusiveSum)
+  BB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(P->scan_tmp, tmp, d_dpre, d_dpre, (int)dwords, st));
+  BB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(P->scan_tmp, tmp, d_spre, d_spre, (int)swords, st));
+  count_launch(2);
+  // node counts per job -> host
+  if ((size_t)(4 * nj + 8) > P->h_cap) {
+    if (P->h_pin) cudaFreeHost(P->h_pin);
+    BB_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P->h_pin), 16 * nj + 64, cudaHostAllocDefault));
+    P->h_cap = 4 * nj + 8;
+  }
+  std::vector<uint64_t> need_idx;
+  for (int i = 0; i < nj; i++) {
+    // count = prefix[next job's first word] - prefix[first word]; last words are padding (zero)
+    uint64_t dend = J[i].dbm + (J[i].n + 3) / 4;
+    uint64_t send = J[i].sbm + (J[i].n + 31) / 32 + 1;
+    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i, d_dpre + J[i].dbm, 4, cudaMemcpyDeviceToHost, st));
+    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i + 1, d_dpre + dend, 4, cudaMemcpyDeviceToHost, st));
+    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i + 2, d_spre + J[i].sbm, 4, cudaMemcpyDeviceToHost, st));
+    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i + 3, d_spre + send, 4, cudaMemcpyDeviceToHost, st));
+  }
+  BB_CUDA_TRY(cudaStreamSynchronize(st));
+  uint32_t nnodes = 0;
+  std::vector<uint32_t> node_job;
+  for (int i = 0; i < nj; i++) {
+    J[i].ndyn = P->h_pin[4 * i + 1] - P->h_pin[4 * i];
+    J[i].nsto = P->h_pin[4 * i + 3] - P->h_pin[4 * i + 2];
+    J[i].node0 = nnodes;
+    uint32_t cnt = 1 + J[i].ndyn + 2 * J[i].nsto;
+    nnodes += cnt;
+    node_job.insert(node_job.end(), cnt, (uint32_t)i);
+  }
+  int levels = 1;
+  while ((1u << levels) <= nnodes + 1) levels++;
+  size_t need2 = al(sizeof(Node) * nnodes) + al(4 * nnodes) + al(4ull * nnodes * levels) + al(4 * nnodes) +
+                 2 * al(8 * nnodes) + 4096;
+  Workspace& nodesw = P->nodesw;
+  rc = nodesw.reserve(need2);
+  if (rc) return rc;
+  Node* d_nodes = nodesw.take<Node>(nnodes);
+  uint32_t* d_node_job = nodesw.take<uint32_t>(nnodes);
+  uint32_t* d_jump = nodesw.take<uint32_t>((size_t)nnodes * levels);
+  uint32_t* d_chain_nodes = nodesw.take<uint32_t>(nnodes);
+  uint64_t* d_out_off = nodesw.take<uint64_t>(nnodes);
+  uint64_t* d_m_off = nodesw.take<uint64_t>(nnodes);
+  BB_CUDA_TRY(cudaMemcpyAsync(d_jobs, J.data(), sizeof(PJob) * nj, cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_node_job, node_job.data(), 4 * nnodes, cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemsetAsync(d_nodes, 0, sizeof(Node) * nnodes, st));
+  // P2
+  {
+    dim3 g(grid_for(dwords + swords, 256, 8), nj);
+    k_node_positions<<<g, 256, 0, st>>>(d_jobs, nj, d_dbm, d_dpre, d_sbm, d_spre, d_nodes);
+    BB_LAUNCH_CHECK();
+  }
+  T.mark("inflate.decode_nodes");
+  k_decode_nodes<<<(nnodes + ND_THREADS - 1) / ND_THREADS, ND_THREADS, nd_smem, st>>>(d_jobs, d_node_job, nnodes,
+                                                                                      d_nodes);
+  BB_LAUNCH_CHECK();
+  T.mark("inflate.link_chain");
+  // P3, P4
+  k_link<<<(nnodes + 255) / 256, 256, 0, st>>>(d_jobs, d_node_job, nnodes, d_nodes, d_dbm, d_dpre, d_sbm, d_spre,
+                                               d_jump);
+  BB_LAUNCH_CHECK();
+  for (int k = 1; k < levels; k++) {
+    k_lift<<<(nnodes + 255) / 256, 256, 0, st>>>(d_jump + (size_t)(k - 1) * nnodes, d_jump + (size_t)k * nnodes,
+                                                 nnodes);
+    BB_LAUNCH_CHECK();
+  }
+  k_chain_len<<<(nj + 63) / 64, 64, 0, st>>>(d_jobs, nj, d_jump, nnodes, levels, d_chains);
+  BB_LAUNCH_CHECK();
+  {
+    dim3 g(std::max<unsigned>(1, std::min<unsigned>((nnodes + 255) / 256, 4096)), nj);
+    k_chain_nodes<<<g, 256, 0, st>>>(d_jobs, d_chains, d_jump, nnodes, levels, d_chain_nodes);
+    BB_LAUNCH_CHECK();
+  }
+  k_chain_scan<<<nj, 256, 0, st>>>(d_jobs, d_chains, d_chain_nodes, d_nodes, d_out_off, d_m_off, d_totals);
+  BB_LAUNCH_CHECK();
+  // chain lengths to the host for the per-block launches
+  std::vector<Chain> hc(nj);
+  BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin, d_chains, std::min<size_t>(sizeof(Chain) * nj, 16 * nj + 64),
+                              cudaMemcpyDeviceToHost, st));
+  BB_CUDA_TRY(cudaStreamSynchronize(st));
+  std::memcpy(hc.data(), P->h_pin, sizeof(Chain) * nj);
+  std::vector<uint32_t> emit_job, emit_base(nj), copy_job, copy_base(nj);
+  for (int i = 0; i < nj; i++) {
+    emit_base[i] = (uint32_t)emit_job.size();
+    emit_job.insert(emit_job.end(), (hc[i].len + ND_THREADS - 1) / ND_THREADS, (uint32_t)i);
+    copy_base[i] = (uint32_t)copy_job.size();
+    copy_job.insert(copy_job.end(), hc[i].len, (uint32_t)i);
+  }
+  Workspace& lists = P->lists;
+  rc = lists.reserve(4 * (emit_job.size() + copy_job.size() + 2 * nj) + 4096);
+  if (rc) return rc;
+  uint32_t* d_emit_job = lists.take<uint32_t>(emit_job.size() + 1);
+  uint32_t* d_emit_base = lists.take<uint32_t>(nj);
+  uint32_t* d_copy_job = lists.take<uint32_t>(copy_job.size() + 1);
+  uint32_t* d_copy_base = lists.take<uint32_t>(nj);
+  if (!emit_job.empty())
+    BB_CUDA_TRY(cudaMemcpyAsync(d_emit_job, emit_job.data(), 4 * emit_job.size(), cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_emit_base, emit_base.data(), 4 * nj, cudaMemcpyHostToDevice, st));
+  if (!copy_job.empty())
+    BB_CUDA_TRY(cudaMemcpyAsync(d_copy_job, copy_job.data(), 4 * copy_job.size(), cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_copy_base, copy_base.data(), 4 * nj, cudaMemcpyHostToDevice, st));
+  // P5
+  T.mark("inflate.emit");
+  if (!emit_job.empty()) {
+    k_emit_nodes<<<(unsigned)emit_job.size(), ND_THREADS, nd_smem, st>>>(d_jobs, nj, d_chains, d_chain_nodes,
+                                                                         d_emit_job, d_emit_base, d_nodes, d_out_off,
+                                                                         d_m_off, d_matches, d_fail);
+    BB_LAUNCH_CHECK();
+  }
+  if (!copy_job.empty()) {
+    k_copy_stored<<<(unsigned)copy_job.size(), 256, 0, st>>>(d_jobs, d_chains, d_chain_nodes, d_nodes, d_out_off,
+                                                             d_copy_job, d_copy_base);
+    BB_LAUNCH_CHECK();
+  }
+  k_tail<<<(nj + 31) / 32, 32, 0, st>>>(d_jobs, nj, d_chains, d_nodes, d_totals, d_matches, d_fail, d_out_total,
+                                        d_want, d_tabs);
+  BB_LAUNCH_CHECK();
+  // P6
+  T.mark("inflate.resolve");
+  if (!sub_job.empty()) {
+    k_resolve_local<<<(unsigned)sub_job.size(), RS_THREADS, SUB * 4, st>>>(d_jobs, d_sub_job, d_out_total, d_fail,
+                                                                     d_matches, d_ext, d_ext_cnt);
+    BB_LAUNCH_CHECK();
+    k_resolve_ext<<<nj, 1024, 0, st>>>(d_jobs, d_out_total, d_fail, d_ext, d_ext_cnt);
+    BB_LAUNCH_CHECK();
+  }
+  // P7
+  T.mark("inflate.adler");
+  if (!chunk_job.empty()) {
+    k_adler_part<<<(unsigned)chunk_job.size(), PA_THREADS, 0, st>>>(d_jobs, d_chunk_job, d_chunk_base, d_part);
+    BB_LAUNCH_CHECK();
+  }
+  k_adler_check<<<(nj + 63) / 64, 64, 0, st>>>(d_jobs, nj, d_chunk_base, d_part, d_want, d_fail);
+  BB_LAUNCH_CHECK();
+  BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin, d_fail, 4 * nj, cudaMemcpyDeviceToHost, st));
+  BB_CUDA_TRY(cudaStreamSynchronize(st));
+  T.finish();
+  for (int i = 0; i < nj; i++) ok[i] = P->h_pin[i] == 0;
+  return BB_OK;
+}
+
+}  // namespace bb

@@ -67,4 +67,10 @@ void inflate_engine_destroy(InflateEngine* e);
 // Synchronizes `st`; status[i] = BB_OK or BB_CORRUPT_CONTAINER (uncompress parity).
 int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStream_t st, int* status);
 
+// bb_inflate_par.cu: the parallel fast path (ok[i] = 1 when fully validated)
+struct ParInflate;
+ParInflate* par_inflate_create();
+void par_inflate_destroy(ParInflate* p);
+int par_inflate(ParInflate* p, const std::vector<InflateJob>& jobs, cudaStream_t st, int* ok);
+
 }  // namespace bb

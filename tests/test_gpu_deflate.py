@@ -154,3 +154,55 @@ def test_container_roundtrip_golden_inputs(codec, golden, oracle):
         data = data[: len(data) // 2 * 2]
         c = oracle.compress(data, 1, e["split"])
         assert codec.decompress_serialized(c) == data
+
+
+def _inflate_counts():
+    from paper_2604_21072_b200 import _lib
+    L = _lib.load()
+    out = (C.c_uint64 * 3)()
+    L.bb_debug_inflate_counts(out)
+    return list(out)
+
+
+def test_parallel_inflate_large_streams(codec, oracle):
+    """Streams >= 64 KiB take the parallel decoder; it must validate them itself
+    (no silent fallback) and reproduce the input exactly."""
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    cases = [oracle.synth_fp16(600000, 1)[1::2], oracle.synth_fp16(600000, 1)[0::2],
+             oracle.synth_bf16(700000, 2)[1::2], oracle.synth_bf16(300000, 3),
+             np.random.default_rng(4).integers(0, 64, 500000, dtype=np.uint8).tobytes(),
+             random.Random(5).randbytes(300000), b"\x42" * 400000,
+             make_input("runs:400000:6"), make_input("period:300000:7:300")]
+    for data in cases:
+        for level in (6, 1, 9):
+            blob = zlib.compress(data, level)
+            if len(blob) < (1 << 16):
+                continue
+            before = _inflate_counts()
+            assert dec(blob, len(data)) == data
+            after = _inflate_counts()
+            assert after[0] == before[0] + 1, (len(data), level, before, after)
+
+
+def test_parallel_inflate_rejects_corruption(codec, oracle):
+    from oracle.oracle import OracleError
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    data = oracle.synth_bf16(200000, 8)
+    base = zlib.compress(data, 6)
+    rng = random.Random(9)
+    for trial in range(40):
+        blob = bytearray(base)
+        for _ in range(1 + rng.randrange(4)):
+            blob[rng.randrange(len(blob))] ^= 1 << rng.randrange(8)
+        blob = bytes(blob)
+        try:
+            want_ok = len(oracle.zlib_uncompress(blob, len(data))) == len(data)
+        except OracleError:
+            want_ok = False
+        try:
+            got = dec(blob, len(data))
+            assert got == data or want_ok
+            got_ok = True
+        except codec.CorruptContainer:
+            got_ok = False
+        assert got_ok == want_ok
