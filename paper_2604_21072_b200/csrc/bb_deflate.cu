@@ -181,6 +181,27 @@ __device__ __forceinline__ uint64_t slides_at(uint64_t t, uint64_t n) {
 // within 32767).  One warp per segment; a 64 KiB u16 head table in shared
 // memory; positions are inserted in order, 32 at a time, with __match_any_sync
 // resolving same-hash lanes inside the warp.
+__device__ __forceinline__ void hp_load_tile(const uint8_t* src, uint64_t n, uint64_t c, int lane, uint32_t& w,
+                                             uint32_t& x) {
+  // lane holds bytes [c + 4 lane, c + 4 lane + 4); x = bytes [c + 128, c + 132)
+  uint64_t a = c + 4 * (uint64_t)lane;
+  w = 0;
+#pragma unroll
+  for (int t = 0; t < 4; t++)
+    if (a + t < n) w |= (uint32_t)__ldg(src + a + t) << (8 * t);
+  x = 0;
+#pragma unroll
+  for (int t = 0; t < 4; t++)
+    if (c + 128 + t < n) x |= (uint32_t)__ldg(src + c + 128 + t) << (8 * t);
+}
+
+__device__ __forceinline__ uint32_t hp_byte(uint32_t w, uint32_t x, uint32_t i) {
+  // byte i (0..131) of the current tile
+  uint32_t v = __shfl_sync(0xffffffffu, w, (i >> 2) & 31);
+  if (i >= 128) v = x;
+  return (v >> (8 * (i & 3))) & 0xff;
+}
+
 __global__ void __launch_bounds__(32) k_hash_prev(const LaneDev* __restrict__ lanes,
                                                   const WorkItem* __restrict__ work,
                                                   uint16_t* __restrict__ pd) {
@@ -197,29 +218,39 @@ __global__ void __launch_bounds__(32) k_hash_prev(const LaneDev* __restrict__ la
   __syncwarp();
   const uint8_t* src = L.src;
   uint16_t* out = pd + L.pbase;
-  for (uint64_t c = base; c < e; c += 32) {
-    uint64_t q = c + lane;
-    bool valid = q < e && q + MIN_MATCH <= n;
-    uint32_t h = 0x10000u + lane;
-    if (valid) h = (((uint32_t)src[q] << 10) ^ ((uint32_t)src[q + 1] << 5) ^ src[q + 2]) & 0x7fff;
-    unsigned peers = __match_any_sync(0xffffffffu, h);
-    unsigned lower = peers & ((1u << lane) - 1);
-    uint32_t d = 0;
-    if (valid) {
-      if (lower) {
-        d = lane - (31 - __clz(lower));
-      } else {
-        uint32_t r = head[h];
-        if (r) {
-          uint64_t dd = q - (base + r - 1);
-          d = dd < WSIZE ? (uint32_t)dd : 0;
+  uint32_t wc, xc;
+  hp_load_tile(src, n, base, lane, wc, xc);
+  for (uint64_t c = base; c < e; c += 128) {
+    uint32_t wn = 0, xn = 0;
+    if (c + 128 < e) hp_load_tile(src, n, c + 128, lane, wn, xn);  // prefetch the next tile
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t i = 32 * k + lane;
+      const uint64_t q = c + i;
+      const uint32_t b0 = hp_byte(wc, xc, i), b1 = hp_byte(wc, xc, i + 1), b2 = hp_byte(wc, xc, i + 2);
+      const bool valid = q < e && q + MIN_MATCH <= n;
+      uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
+      unsigned peers = __match_any_sync(0xffffffffu, h);
+      unsigned lower = peers & ((1u << lane) - 1);
+      uint32_t d = 0;
+      if (valid) {
+        if (lower) {
+          d = lane - (31 - __clz(lower));
+        } else {
+          uint32_t r = head[h];
+          if (r) {
+            uint64_t dd = q - (base + r - 1);
+            d = dd < WSIZE ? (uint32_t)dd : 0;
+          }
         }
       }
+      __syncwarp();
+      if (valid && (peers >> lane) == 1u) head[h] = (uint16_t)(q - base + 1);
+      __syncwarp();
+      if (q >= s && q < e) out[q] = (uint16_t)d;
     }
-    __syncwarp();
-    if (valid && (peers >> lane) == 1u) head[h] = (uint16_t)(q - base + 1);
-    __syncwarp();
-    if (q >= s && q < e) out[q] = (uint16_t)d;
+    wc = wn;
+    xc = xn;
   }
 }
 
@@ -544,99 +575,117 @@ struct BlockCodes {
   uint32_t d[D_CODES];
 };
 
-struct TreeSmem {
-  uint16_t freq[HEAP_SIZE];
-  uint16_t dad[HEAP_SIZE];
-  uint16_t len[HEAP_SIZE + 1];
-  uint16_t code[HEAP_SIZE];
+// zlib trees.c state for one block.  The heap holds packed entries
+// (freq << 32 | depth << 16 | node): zlib's smaller() order -- freq, then depth
+// -- is the order of (entry >> 16), so each heap step is one 64-bit compare
+// instead of four indirect loads.
+template <int ELEMS>
+struct TreeArr {
+  uint16_t freq[ELEMS];
+  uint16_t code[ELEMS];
+  uint16_t dad[2 * ELEMS + 1];
+  uint16_t len[2 * ELEMS + 2];  // +1: scan_tree guard slot
 };
 
 struct TreesState {
-  TreeSmem lt, dt, blt;
+  TreeArr<L_CODES> lt;
+  TreeArr<D_CODES> dt;
+  TreeArr<BL_CODES> blt;
+  uint64_t heap[HEAP_SIZE];
   uint16_t bl_count[16];
-  int heap_len, heap_max;
   uint64_t opt_len, static_len;
   int lmax, dmax, blmax;
-  int16_t heap[HEAP_SIZE];
-  uint8_t depth[HEAP_SIZE];
 };
 
-__device__ __forceinline__ bool t_smaller(const uint16_t* freq, int n, int m, const uint8_t* depth) {
-  return freq[n] < freq[m] || (freq[n] == freq[m] && depth[n] <= depth[m]);
+__device__ __forceinline__ uint64_t t_entry(uint32_t freq, uint32_t depth, uint32_t node) {
+  return ((uint64_t)freq << 32) | (depth << 16) | node;
 }
+__device__ __forceinline__ uint32_t t_node(uint64_t e) { return (uint32_t)(e & 0xffff); }
+__device__ __forceinline__ uint32_t t_freq(uint64_t e) { return (uint32_t)(e >> 32); }
+__device__ __forceinline__ uint32_t t_depth(uint64_t e) { return (uint32_t)((e >> 16) & 0xffff); }
 
-__device__ void t_pqdownheap(TreesState* s, const uint16_t* freq, int k) {
-  int v = s->heap[k];
+// trees.c pqdownheap with smaller(n, m) == key(n) <= key(m)
+__device__ __forceinline__ void t_down(uint64_t* heap, int heap_len, int k) {
+  const uint64_t v = heap[k];
+  const uint64_t vk = v >> 16;
   int j = k << 1;
-  while (j <= s->heap_len) {
-    if (j < s->heap_len && t_smaller(freq, s->heap[j + 1], s->heap[j], s->depth)) j++;
-    if (t_smaller(freq, v, s->heap[j], s->depth)) break;
-    s->heap[k] = s->heap[j];
+  while (j <= heap_len) {
+    uint64_t hj = heap[j];
+    if (j < heap_len) {
+      uint64_t hj1 = heap[j + 1];
+      if ((hj1 >> 16) <= (hj >> 16)) {
+        j++;
+        hj = hj1;
+      }
+    }
+    if (vk <= (hj >> 16)) break;
+    heap[k] = hj;
     k = j;
     j <<= 1;
   }
-  s->heap[k] = (int16_t)v;
+  heap[k] = v;
 }
 
 // trees.c build_tree + gen_bitlen + gen_codes (single thread)
-// kind: 0 lit/len, 1 dist, 2 bit-length
-__device__ int t_build_tree(TreesState* s, TreeSmem* t, int kind) {
-  const int elems = kind == 0 ? L_CODES : kind == 1 ? D_CODES : BL_CODES;
-  const int max_length = kind == 2 ? 7 : 15;
-  const int base = kind == 0 ? 257 : 0;
-  int n, m, max_code = -1, node;
-  s->heap_len = 0;
-  s->heap_max = HEAP_SIZE;
-  for (n = 0; n < elems; n++) {
+// KIND: 0 lit/len, 1 dist, 2 bit-length
+template <int KIND, int ELEMS>
+__device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
+  constexpr int max_length = KIND == 2 ? 7 : 15;
+  constexpr int base = KIND == 0 ? 257 : 0;
+  uint64_t* heap = s->heap;
+  int n, max_code = -1, node;
+  int heap_len = 0, heap_max = HEAP_SIZE;
+  for (n = 0; n < ELEMS; n++) {
     if (t->freq[n] != 0) {
-      s->heap[++(s->heap_len)] = (int16_t)(max_code = n);
-      s->depth[n] = 0;
+      heap[++heap_len] = t_entry(t->freq[n], 0, n);
+      max_code = n;
     } else {
       t->len[n] = 0;
     }
   }
-  while (s->heap_len < 2) {
-    node = s->heap[++(s->heap_len)] = (int16_t)(max_code < 2 ? ++max_code : 0);
+  while (heap_len < 2) {
+    node = max_code < 2 ? ++max_code : 0;
+    heap[++heap_len] = t_entry(1, 0, node);
     t->freq[node] = 1;
-    s->depth[node] = 0;
     s->opt_len--;
-    if (kind == 0) s->static_len -= c_z.sl_len[node];
-    else if (kind == 1) s->static_len -= 5;
+    if (KIND == 0) s->static_len -= c_z.sl_len[node];
+    else if (KIND == 1) s->static_len -= 5;
   }
-  for (n = s->heap_len / 2; n >= 1; n--) t_pqdownheap(s, t->freq, n);
-  node = elems;
+  for (n = heap_len / 2; n >= 1; n--) t_down(heap, heap_len, n);
+  node = ELEMS;
   do {
-    n = s->heap[1];
-    s->heap[1] = s->heap[s->heap_len--];
-    t_pqdownheap(s, t->freq, 1);
-    m = s->heap[1];
-    s->heap[--(s->heap_max)] = (int16_t)n;
-    s->heap[--(s->heap_max)] = (int16_t)m;
-    t->freq[node] = (uint16_t)(t->freq[n] + t->freq[m]);
-    s->depth[node] = (uint8_t)((s->depth[n] >= s->depth[m] ? s->depth[n] : s->depth[m]) + 1);
-    t->dad[n] = t->dad[m] = (uint16_t)node;
-    s->heap[1] = (int16_t)(node++);
-    t_pqdownheap(s, t->freq, 1);
-  } while (s->heap_len >= 2);
-  s->heap[--(s->heap_max)] = s->heap[1];
+    const uint64_t en = heap[1];
+    heap[1] = heap[heap_len--];
+    t_down(heap, heap_len, 1);
+    const uint64_t em = heap[1];
+    heap[--heap_max] = en;
+    heap[--heap_max] = em;
+    const uint32_t f = t_freq(en) + t_freq(em);
+    const uint32_t d = max(t_depth(en), t_depth(em)) + 1;
+    t->dad[t_node(en)] = t->dad[t_node(em)] = (uint16_t)node;
+    heap[1] = t_entry(f & 0xffff, d, node);  // ush Freq, as in zlib
+    node++;
+    t_down(heap, heap_len, 1);
+  } while (heap_len >= 2);
+  heap[--heap_max] = heap[1];
 
   // gen_bitlen
   int h, bits, overflow = 0;
   for (bits = 0; bits <= 15; bits++) s->bl_count[bits] = 0;
-  t->len[s->heap[s->heap_max]] = 0;
-  for (h = s->heap_max + 1; h < (int)HEAP_SIZE; h++) {
-    n = s->heap[h];
+  t->len[t_node(heap[heap_max])] = 0;
+  for (h = heap_max + 1; h < (int)HEAP_SIZE; h++) {
+    n = t_node(heap[h]);
     bits = t->len[t->dad[n]] + 1;
     if (bits > max_length) bits = max_length, overflow++;
     t->len[n] = (uint16_t)bits;
     if (n > max_code) continue;
     s->bl_count[bits]++;
     int xbits = 0;
-    if (n >= base) xbits = kind == 0 ? c_extra_lbits[n - base] : kind == 1 ? c_extra_dbits[n - base] : c_extra_blbits[n - base];
+    if (n >= base) xbits = KIND == 0 ? c_extra_lbits[n - base] : KIND == 1 ? c_extra_dbits[n - base] : c_extra_blbits[n - base];
     uint32_t f = t->freq[n];
     s->opt_len += (uint64_t)f * (uint32_t)(bits + xbits);
-    if (kind == 0) s->static_len += (uint64_t)f * (uint32_t)(c_z.sl_len[n] + xbits);
-    else if (kind == 1) s->static_len += (uint64_t)f * (uint32_t)(5 + xbits);
+    if (KIND == 0) s->static_len += (uint64_t)f * (uint32_t)(c_z.sl_len[n] + xbits);
+    else if (KIND == 1) s->static_len += (uint64_t)f * (uint32_t)(5 + xbits);
   }
   if (overflow) {
     do {
@@ -650,7 +699,7 @@ __device__ int t_build_tree(TreesState* s, TreeSmem* t, int kind) {
     for (bits = max_length; bits != 0; bits--) {
       n = s->bl_count[bits];
       while (n != 0) {
-        m = s->heap[--h];
+        int m = t_node(heap[--h]);
         if (m > max_code) continue;
         if ((uint32_t)t->len[m] != (uint32_t)bits) {
           s->opt_len += ((uint64_t)bits - t->len[m]) * t->freq[m];
@@ -670,14 +719,13 @@ __device__ int t_build_tree(TreesState* s, TreeSmem* t, int kind) {
   for (n = 0; n <= max_code; n++) {
     int l = t->len[n];
     if (l == 0) continue;
-    uint32_t cd = next_code[l]++, r = 0;
-    for (int b = 0; b < l; b++) r = (r << 1) | ((cd >> b) & 1);
-    t->code[n] = (uint16_t)r;
+    t->code[n] = (uint16_t)(__brev((uint32_t)next_code[l]++) >> (32 - l));
   }
   return max_code;
 }
 
-__device__ void t_scan_tree(TreesState* s, TreeSmem* t, int max_code) {
+template <int ELEMS>
+__device__ void t_scan_tree(TreesState* s, TreeArr<ELEMS>* t, int max_code) {
   int prevlen = -1, curlen, nextlen = t->len[0], count = 0, max_count = 7, min_count = 4;
   if (nextlen == 0) max_count = 138, min_count = 3;
   t->len[max_code + 1] = 0xffff;
@@ -717,10 +765,11 @@ struct HdrWriter {
   }
 };
 
-__device__ void t_send_tree(TreesState* s, TreeSmem* t, int max_code, HdrWriter& hw) {
+template <int ELEMS>
+__device__ void t_send_tree(TreesState* s, TreeArr<ELEMS>* t, int max_code, HdrWriter& hw) {
   int prevlen = -1, curlen, nextlen = t->len[0], count = 0, max_count = 7, min_count = 4;
   if (nextlen == 0) max_count = 138, min_count = 3;
-  TreeSmem* bl = &s->blt;
+  TreeArr<BL_CODES>* bl = &s->blt;
   for (int n = 0; n <= max_code; n++) {
     curlen = nextlen;
     nextlen = t->len[n + 1];
@@ -752,7 +801,7 @@ __device__ void t_send_tree(TreesState* s, TreeSmem* t, int max_code, HdrWriter&
   }
 }
 
-constexpr int BK_THREADS = 256;
+constexpr int BK_THREADS = 64;
 
 __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict__ lanes,
                                                        const uint32_t* __restrict__ blk_lane,
@@ -779,11 +828,7 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   const uint64_t s1 = (b == L.nblk - 1) ? L.total : s0 + SYM_LIMIT;
   const uint32_t nsym = (uint32_t)(s1 - s0);
   // init (init_block: END_BLOCK freq 1)
-  for (int i = threadIdx.x; i < (int)HEAP_SIZE; i += blockDim.x) {
-    S.lt.freq[i] = 0;
-    S.dt.freq[i] = 0;
-    S.blt.freq[i] = 0;
-  }
+  for (int i = threadIdx.x; i < (int)BL_CODES; i += blockDim.x) S.blt.freq[i] = 0;
   for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) h_l[i] = 0;
   for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) h_d[i] = 0;
   for (int i = threadIdx.x; i < (int)(HDR_BYTES / 4); i += blockDim.x) hw_buf[i] = 0;
@@ -817,11 +862,11 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   if (threadIdx.x == 0) {
     S.opt_len = 0;
     S.static_len = 0;
-    S.lmax = t_build_tree(&S, &S.lt, 0);
-    S.dmax = t_build_tree(&S, &S.dt, 1);
+    S.lmax = t_build_tree<0>(&S, &S.lt);
+    S.dmax = t_build_tree<1>(&S, &S.dt);
     t_scan_tree(&S, &S.lt, S.lmax);
     t_scan_tree(&S, &S.dt, S.dmax);
-    t_build_tree(&S, &S.blt, 2);
+    t_build_tree<2>(&S, &S.blt);
     int max_blindex;
     for (max_blindex = BL_CODES - 1; max_blindex >= 3; max_blindex--)
       if (S.blt.len[c_bl_order[max_blindex]] != 0) break;
