@@ -264,62 +264,74 @@ __device__ __forceinline__ uint32_t prof_pack(uint32_t best, uint32_t bestd) {
   return best | (bestd << 9);
 }
 
+// Shared-memory window word per position q: bits 0-15 prev-same-hash distance,
+// bits 16-23 byte q, bits 24-31 byte q+1.  One 32-bit load yields a chain link
+// and a byte pair, so a chain step costs two loads: the candidate's word (link
+// + bytes 0,1) and the word at candidate + best_len - 1 (bytes best-1, best --
+// zlib's scan_end1 / scan_end quick reject).
+constexpr uint32_t PF_WIN = WSIZE + PF_SEG + MAX_MATCH + 32;
+
 __global__ void __launch_bounds__(PF_THREADS, 1) k_profile(const LaneDev* __restrict__ lanes,
                                                            const WorkItem* __restrict__ work,
                                                            const uint16_t* __restrict__ pd,
                                                            uint2* __restrict__ prof) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(16) uint32_t w32[];
   const WorkItem w = work[blockIdx.x];
   const LaneDev L = lanes[w.lane];
   const uint64_t n = L.n;
   const uint64_t s = w.start;
   const uint64_t e = umin64(s + PF_SEG, n);
   const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
-  const uint64_t whi = umin64(e + MAX_MATCH + 16, n);
-  const uint32_t wlen = (uint32_t)(whi - wlo);
-  const uint32_t plen = (uint32_t)(e - wlo);  // links needed for [wlo, e)
-  uint8_t* win = smem;                                                  // wlen (+16 slack)
-  uint16_t* lnk = reinterpret_cast<uint16_t*>(smem + ((WSIZE + PF_SEG + MAX_MATCH + 32 + 15) & ~15u));
-  // stage bytes (16 B gathers) and links
-  const uint8_t* src = L.src + wlo;
-  for (uint32_t i = threadIdx.x; i < wlen / 16; i += blockDim.x) {
-    uint32_t v[4];
-    gather16(src + 16 * i, v);
-    reinterpret_cast<uint4*>(win)[i] = make_uint4(v[0], v[1], v[2], v[3]);
+  const uint32_t wlen = (uint32_t)(e - wlo) + MAX_MATCH + 16;  // <= PF_WIN
+  const uint8_t* src = L.src;
+  const uint16_t* pdl = pd + L.pbase;
+  for (uint32_t i = threadIdx.x; i < wlen; i += blockDim.x) {
+    const uint64_t q = wlo + i;
+    uint32_t v = q < e ? pdl[q] : 0;
+    if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
+    if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
+    w32[i] = v;
   }
-  for (uint32_t i = (wlen & ~15u) + threadIdx.x; i < wlen; i += blockDim.x) win[i] = src[i];
-  const uint16_t* pdl = pd + L.pbase + wlo;
-  for (uint32_t i = threadIdx.x; i < plen; i += blockDim.x) lnk[i] = pdl[i];
   __syncthreads();
 
   for (uint64_t p = s + threadIdx.x; p < e; p += blockDim.x) {
     const uint32_t ip = (uint32_t)(p - wlo);
-    uint32_t d0 = lnk[ip];
+    const uint32_t wp = w32[ip];
+    const uint32_t d0 = wp & 0xffff;
     uint2 res = make_uint2(0, 0);
     if (p + MIN_MATCH <= n && d0 != 0 && d0 <= MAX_DIST && p != d0) {
       const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
       const uint32_t nice = min(NICE_LENGTH, la);
       const uint32_t maxl = min(MAX_MATCH, la);
       const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
+      const uint32_t lim_rel = limit > wlo ? (uint32_t)(limit - wlo) : 0;  // candidates need ic > lim_rel
+      const bool lim_any = limit >= wlo;  // lim_rel meaningful (else only ic >= 0 needed... see below)
       const uint32_t flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
-      const uint8_t* sp = win + ip;
-      const uint8_t s0 = sp[0], s1 = sp[1];
+      const uint32_t s01 = wp >> 16;
       uint32_t best = MIN_MATCH - 1, bestd = 0, cnt = 0, r32 = 0;
       bool r32_set = false;
-      uint8_t se1 = sp[best - 1], se = sp[best];
-      uint32_t ic = ip - d0;  // candidate, window-relative
+      uint32_t se01 = w32[ip + best - 1] >> 16;
+      uint32_t ic = ip - d0;
       for (;;) {
         cnt++;
-        const uint8_t* mp = win + ic;
-        if (mp[best] == se && mp[best - 1] == se1 && mp[0] == s0 && mp[1] == s1) {
+        const uint32_t wc = w32[ic];
+        const uint32_t we = w32[ic + best - 1];
+        if ((wc >> 16) == s01 && (we >> 16) == se01) {
           uint32_t len = 2;
-          while (len < maxl && mp[len] == sp[len]) len++;
+          while (len < maxl) {
+            uint32_t x = (w32[ic + len] ^ w32[ip + len]) >> 16;
+            if (x) {
+              len += (x & 0xff) == 0;
+              break;
+            }
+            len += 2;
+          }
+          len = min(len, maxl);
           if (len > best) {
             best = len;
             bestd = ip - ic;
             if (len >= nice) break;
-            se1 = sp[best - 1];
-            se = sp[best];
+            se01 = w32[ip + best - 1] >> 16;
           }
         }
         if (cnt == 32) {
@@ -327,10 +339,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile(const LaneDev* __rest
           r32_set = true;
         }
         if (cnt == MAX_CHAIN) break;
-        uint32_t dd = lnk[ic];
+        const uint32_t dd = wc & 0xffff;
         if (dd == 0 || dd > ic) break;
-        uint32_t nx = ic - dd;
-        if (wlo + nx <= limit) break;
+        const uint32_t nx = ic - dd;
+        if (lim_any ? nx <= lim_rel : false) break;
         ic = nx;
       }
       if (!r32_set) r32 = prof_pack(best, bestd);
@@ -1394,7 +1406,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     ZTables t = make_tables();
     BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
     e->tables_ready = true;
   }
   const int nl = (int)jobs.size();
@@ -1527,7 +1539,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   }
   T.mark("deflate.profile");
   if (!pf_work.empty()) {
-    size_t smem = ((WSIZE + PF_SEG + MAX_MATCH + 32 + 15) & ~15u) + 2 * (WSIZE + PF_SEG);
+    size_t smem = 4 * PF_WIN;
     k_profile<<<(unsigned)pf_work.size(), PF_THREADS, smem, st>>>(d_lanes, d_pf, d_pd, d_prof);
     BB_LAUNCH_CHECK();
   }
@@ -1630,7 +1642,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   ZTables t = make_tables();
   BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-  BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
   LaneDev d{};
   d.src = d_in;
   d.n = n;
@@ -1650,7 +1662,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
     BB_LAUNCH_CHECK();
   }
   if (!pf.empty() && d_prof) {
-    size_t smem = ((WSIZE + PF_SEG + MAX_MATCH + 32 + 15) & ~15u) + 2 * (WSIZE + PF_SEG);
+    size_t smem = 4 * PF_WIN;
     k_profile<<<(unsigned)pf.size(), PF_THREADS, smem, st>>>(dl, dp, d_pd, reinterpret_cast<uint2*>(d_prof));
     BB_LAUNCH_CHECK();
   }

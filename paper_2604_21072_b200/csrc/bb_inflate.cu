@@ -395,9 +395,20 @@ int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStr
     }
   }
   if (!big.empty()) {
+    // pass A: stored-block chains only (cheap); pass B: full candidate search for the rest
     std::vector<int> ok(big.size());
-    int rc = par_inflate(e->par, big, st, ok.data());
+    int rc = par_inflate(e->par, big, st, ok.data(), 0);
     if (rc) return rc;
+    std::vector<InflateJob> dyn;
+    std::vector<size_t> dyn_k;
+    for (size_t k = 0; k < big.size(); k++)
+      if (!ok[k]) dyn.push_back(big[k]), dyn_k.push_back(k);
+    if (!dyn.empty()) {
+      std::vector<int> ok2(dyn.size());
+      rc = par_inflate(e->par, dyn, st, ok2.data(), 1);
+      if (rc) return rc;
+      for (size_t q = 0; q < dyn.size(); q++) ok[dyn_k[q]] = ok2[q];
+    }
     for (size_t k = 0; k < big.size(); k++) {
       if (ok[k]) {
         status[big_idx[k]] = BB_OK;

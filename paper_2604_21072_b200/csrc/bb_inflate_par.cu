@@ -82,25 +82,27 @@ struct Match {
 };
 
 // ---- bit access -------------------------------------------------------------
-__device__ __forceinline__ uint64_t load_le64(const uint8_t* p, uint64_t n, uint64_t byte) {
+__device__ __forceinline__ uint64_t load_le64_slow(const uint8_t* p, uint64_t n, uint64_t byte) {
   uint64_t v = 0;
-  if (byte + 8 <= n) {
-#pragma unroll
-    for (int i = 0; i < 8; i++) v |= (uint64_t)__ldg(p + byte + i) << (8 * i);
-  } else {
-    for (int i = 0; i < 8; i++)
-      if (byte + i < n) v |= (uint64_t)__ldg(p + byte + i) << (8 * i);
-  }
+  for (int i = 0; i < 8; i++)
+    if (byte + i < n) v |= (uint64_t)__ldg(p + byte + i) << (8 * i);
   return v;
 }
 
-// 64 bits starting at bit `b` (zero beyond the end)
+// 64 bits starting at bit `b` (zero beyond the end): two aligned 64-bit loads
 __device__ __forceinline__ uint64_t peek64(const uint8_t* p, uint64_t n, uint64_t b) {
-  uint64_t byte = b >> 3;
-  uint32_t sh = (uint32_t)(b & 7);
-  uint64_t lo = load_le64(p, n, byte);
+  const uint64_t byte = b >> 3;
+  if (byte + 16 <= n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p + byte);
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
+    const uint32_t sh = (uint32_t)(((a & 7) << 3) + (b & 7));  // 0..63
+    const uint64_t lo = __ldg(w), hi = __ldg(w + 1);
+    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+  }
+  const uint32_t sh = (uint32_t)(b & 7);
+  const uint64_t lo = load_le64_slow(p, n, byte);
   if (!sh) return lo;
-  uint64_t hi = byte + 8 < n ? __ldg(p + byte + 8) : 0;
+  const uint64_t hi = byte + 8 < n ? __ldg(p + byte + 8) : 0;
   return (lo >> sh) | (hi << (64 - sh));
 }
 
@@ -313,30 +315,95 @@ __device__ int decode_codes(BitReader& r, const Tables* T, uint64_t& out_len, ui
   }
 }
 
+
+// Exact zlib acceptance of a dynamic block header at bit b (inflate.c TABLE /
+// LENLENS / CODELENS + inftrees.c rules), with early rejection as soon as a
+// partial Kraft sum is over-subscribed.  Never rejects a header zlib accepts.
+__device__ bool verify_dynamic(const uint8_t* p, uint64_t n, uint64_t b) {
+  BitReader r;
+  r.init(p, n, b + 3);
+  uint32_t nlen = r.take(5) + 257, ndist = r.take(5) + 1, ncode = r.take(4) + 4;
+  if (nlen > 286 || ndist > 30) return false;
+  uint8_t cl[19];
+  for (int i = 0; i < 19; i++) cl[i] = 0;
+  for (uint32_t i = 0; i < ncode; i++) cl[p_order[i]] = (uint8_t)r.take(3);
+  HTabT<19> ch;
+  if (htab_build(&ch, cl, 19, 0) || ch.max == 0) return false;
+  Lims L;
+  L.load(&ch);
+  uint32_t have = 0, prev = 0, kl = 0, kd = 0;
+  uint16_t cnt1l = 0, cnt1d = 0, maxl = 0, maxd = 0;
+  bool eob = false;
+  while (have < nlen + ndist) {
+    int sym = hdecode(r, &ch, L);
+    if (sym < 0) return false;
+    uint32_t len, copy;
+    if (sym < 16) {
+      len = (uint32_t)sym;
+      copy = 1;
+    } else if (sym == 16) {
+      if (have == 0) return false;
+      len = prev;
+      copy = 3 + r.take(2);
+    } else if (sym == 17) {
+      len = 0;
+      copy = 3 + r.take(3);
+    } else {
+      len = 0;
+      copy = 11 + r.take(7);
+    }
+    if (have + copy > nlen + ndist) return false;
+    for (uint32_t k = 0; k < copy; k++, have++) {
+      if (!len) continue;
+      if (have < nlen) {
+        kl += 32768u >> len;
+        if (kl > 32768u) return false;
+        if (have == 256) eob = true;
+        maxl = max(maxl, (uint16_t)len);
+        cnt1l += len == 1;
+      } else {
+        kd += 32768u >> len;
+        if (kd > 32768u) return false;
+        maxd = max(maxd, (uint16_t)len);
+        cnt1d += len == 1;
+      }
+    }
+    prev = len;
+    if (r.past_end()) return false;
+  }
+  if (!eob) return false;
+  // incomplete sets are allowed only when the longest code has length 1
+  if (kl != 32768u && maxl != 1) return false;
+  if (kd != 32768u && maxd > 1) return false;
+  return true;
+}
+
 // ---- P1 --------------------------------------------------------------------
 __device__ __forceinline__ uint32_t bits_at(uint64_t w0, uint64_t w1, uint32_t off, uint32_t k) {
   uint64_t v = off < 64 ? (w0 >> off) | (off ? (w1 << (64 - off)) : 0) : (w1 >> (off - 64));
   return (uint32_t)(v & ((1ull << k) - 1));
 }
 
-__device__ __forceinline__ bool dyn_header_ok(const uint8_t* p, uint64_t n, uint64_t b) {
-  if (b + 17 > 8 * n) return false;
-  uint64_t w0 = peek64(p, n, b);
-  if (((w0 >> 1) & 3) != 2) return false;
-  if (((w0 >> 3) & 31) > 29 || ((w0 >> 8) & 31) > 29) return false;
-  uint32_t ncode = (uint32_t)((w0 >> 13) & 15) + 4;
-  uint64_t w1 = peek64(p, n, b + 64);
+// Necessary conditions for a dynamic header at bit `k` of the 128-bit window
+// (w0, w1): BTYPE = 10, HLIT <= 29, HDIST <= 29 and a complete code-length code.
+__device__ __forceinline__ bool dyn_header_quick(uint64_t w0, uint64_t w1, uint32_t k) {
+  const uint64_t x0 = k ? (w0 >> k) | (w1 << (64 - k)) : w0;
+  const uint64_t x1 = w1 >> k;
+  if (((x0 >> 1) & 3) != 2) return false;
+  if (((x0 >> 3) & 31) > 29 || ((x0 >> 8) & 31) > 29) return false;
+  const uint32_t ncode = (uint32_t)((x0 >> 13) & 15) + 4;
   uint32_t kraft = 0;
-  for (uint32_t i = 0; i < ncode; i++) {
-    uint32_t l = bits_at(w0, w1, 17 + 3 * i, 3);
-    if (l) kraft += 128u >> l;
+#pragma unroll
+  for (uint32_t i = 0; i < 19; i++) {
+    const uint32_t l = bits_at(x0, x1, 17 + 3 * i, 3);
+    kraft += (i < ncode && l) ? (128u >> l) : 0u;
   }
   return kraft == 128;
 }
 
 __global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __restrict__ job_of_block,
                              const uint64_t* __restrict__ block_byte0, uint32_t* __restrict__ dbm,
-                             uint32_t* __restrict__ sbm) {
+                             uint32_t* __restrict__ sbm, int find_dynamic) {
   const uint32_t j = job_of_block[blockIdx.x];
   const PJob J = jobs[j];
   const uint64_t B = block_byte0[blockIdx.x] + threadIdx.x;  // one stream byte per thread
@@ -344,9 +411,13 @@ __global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __re
   uint32_t dbits = 0;
   bool st = false;
   if (B < J.n) {
-    for (int k = 0; k < 8; k++) {
-      uint64_t b = 8 * B + k;
-      if (b >= 16 && dyn_header_ok(J.src, J.n, b)) dbits |= 1u << k;
+    if (find_dynamic) {
+      const uint64_t w0 = peek64(J.src, J.n, 8 * B), w1 = peek64(J.src, J.n, 8 * B + 64);
+      for (uint32_t k = 0; k < 8; k++) {
+        const uint64_t b = 8 * B + k;
+        if (b >= 16 && b + 17 <= 8 * J.n && dyn_header_quick(w0, w1, k) && verify_dynamic(J.src, J.n, b))
+          dbits |= 1u << k;
+      }
     }
     if (B >= 2 && B + 4 <= J.n) {
       uint32_t len = __ldg(J.src + B) | ((uint32_t)__ldg(J.src + B + 1) << 8);
@@ -927,7 +998,7 @@ struct ParInflate {
 ParInflate* par_inflate_create() { return new ParInflate(); }
 void par_inflate_destroy(ParInflate* p) { delete p; }
 
-int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t st, int* ok) {
+int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t st, int* ok, int find_dynamic) {
   using namespace par;
   const int nj = (int)jobs.size();
   if (!nj) return BB_OK;
@@ -1014,7 +1085,8 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   BB_CUDA_TRY(cudaMemsetAsync(d_fail, 0, 4 * nj, st));
 
   // P1
-  k_candidates<<<(unsigned)cand_job.size(), 256, 0, st>>>(d_jobs, d_cand_job, d_cand_byte0, d_dbm, d_sbm);
+  k_candidates<<<(unsigned)cand_job.size(), 256, 0, st>>>(d_jobs, d_cand_job, d_cand_byte0, d_dbm, d_sbm,
+                                                          find_dynamic);
   BB_LAUNCH_CHECK();
   k_popc<<<grid_for(dwords, 256, 8), 256, 0, st>>>(d_dbm, dwords, d_dpre);
   BB_LAUNCH_CHECK();

@@ -71,6 +71,8 @@ int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStr
 struct ParInflate;
 ParInflate* par_inflate_create();
 void par_inflate_destroy(ParInflate* p);
-int par_inflate(ParInflate* p, const std::vector<InflateJob>& jobs, cudaStream_t st, int* ok);
+// find_dynamic = 0: only stored blocks are located (a fast first pass that fully
+// decodes lanes made of stored blocks, e.g. incompressible mantissa planes)
+int par_inflate(ParInflate* p, const std::vector<InflateJob>& jobs, cudaStream_t st, int* ok, int find_dynamic);
 
 }  // namespace bb
