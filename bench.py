@@ -52,13 +52,8 @@ def seeds_for(workload: str, rank: int, micro: int) -> int:
 
 def synth(elements: int, seed: int, bf16: bool) -> bytes:
     """Host-side input generator (C++ drop-in, reference synth.cpp semantics)."""
-    import ctypes as C
-    lib = C.CDLL(os.path.join(ROOT, "paper_2604_21072_b200", "libbeeplan_b200.so"))
-    lib.beeplan_synth_gaussian.argtypes = [C.c_size_t, C.c_uint64, C.c_int, C.c_void_p]
-    buf = bytearray(2 * elements)
-    cbuf = (C.c_uint8 * len(buf)).from_buffer(buf)
-    lib.beeplan_synth_gaussian(elements, seed, 1 if bf16 else 0, C.addressof(cbuf))
-    return bytes(buf)
+    from paper_2604_21072_b200 import synth as S
+    return S.gaussian(elements, seed, bf16)
 
 
 def make_inputs(workload: str, rank: int):

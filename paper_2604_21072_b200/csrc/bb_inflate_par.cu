@@ -65,6 +65,8 @@ struct PJob {
   uint64_t mbase;   // match list base
   uint64_t mcap;
   uint32_t sub0, nsub;  // resolution windows
+  uint32_t dyn_base;    // first slot of this job's dynamic nodes in the per-dynamic-node arrays
+  uint64_t xbase;       // first entry of this job's per-output-byte source map
 };
 
 struct Node {
@@ -73,6 +75,13 @@ struct Node {
   uint32_t nmatch;
   uint32_t flags;  // bit0 ok, bit1 final, bit2 stored
   uint64_t start;  // dynamic: header bit; stored: data byte offset (LEN field)
+};
+
+struct Chain {
+  uint32_t len;       // blocks on the chain (excluding the virtual start)
+  uint32_t terminal;  // SENT_END / SENT_BREAK / SENT_BAD
+  uint32_t last;      // last node (the virtual start if len == 0)
+  uint32_t pad;
 };
 
 struct Match {
@@ -401,9 +410,13 @@ __device__ __forceinline__ bool dyn_header_quick(uint64_t w0, uint64_t w1, uint3
   return kraft == 128;
 }
 
+// Survivors of the quick test are appended to a list (warp-aggregated) and
+// verified exactly by k_verify_dynamic with one thread each, so the rare long
+// verifications do not serialise whole warps.
 __global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __restrict__ job_of_block,
                              const uint64_t* __restrict__ block_byte0, uint32_t* __restrict__ dbm,
-                             uint32_t* __restrict__ sbm, int find_dynamic) {
+                             uint32_t* __restrict__ sbm, int find_dynamic, uint64_t* __restrict__ surv,
+                             unsigned long long* __restrict__ surv_cnt, uint64_t surv_cap) {
   const uint32_t j = job_of_block[blockIdx.x];
   const PJob J = jobs[j];
   const uint64_t B = block_byte0[blockIdx.x] + threadIdx.x;  // one stream byte per thread
@@ -415,8 +428,10 @@ __global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __re
       const uint64_t w0 = peek64(J.src, J.n, 8 * B), w1 = peek64(J.src, J.n, 8 * B + 64);
       for (uint32_t k = 0; k < 8; k++) {
         const uint64_t b = 8 * B + k;
-        if (b >= 16 && b + 17 <= 8 * J.n && dyn_header_quick(w0, w1, k) && verify_dynamic(J.src, J.n, b))
-          dbits |= 1u << k;
+        if (b >= 16 && b + 17 <= 8 * J.n && dyn_header_quick(w0, w1, k)) {
+          unsigned long long slot = atomicAdd(surv_cnt, 1ull);
+          if (slot < surv_cap) surv[slot] = ((uint64_t)j << 48) | b;
+        }
       }
     }
     if (B >= 2 && B + 4 <= J.n) {
@@ -425,10 +440,28 @@ __global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __re
       st = len == (~nlen & 0xffff) && B + 4 + len <= J.n;
     }
   }
-  // dynamic bitmap: byte B of the stream -> byte B of the bitmap
-  if (B < J.n) reinterpret_cast<uint8_t*>(dbm + J.dbm)[B] = (uint8_t)dbits;
+  (void)dbits;
   unsigned ball = __ballot_sync(0xffffffffu, st);
   if (lane == 0 && B < J.n + 32) sbm[J.sbm + (B >> 5)] = ball;
+}
+
+
+__global__ void k_verify_dynamic(const PJob* __restrict__ jobs, const uint64_t* __restrict__ surv,
+                                 const unsigned long long* __restrict__ surv_cnt, uint64_t surv_cap,
+                                 uint32_t* __restrict__ dbm, uint32_t* __restrict__ fail, int njobs) {
+  const uint64_t cnt = *surv_cnt;
+  if (cnt > surv_cap) {  // list overflow: let the exact sequential decoder take every job
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < njobs; i += blockDim.x) fail[i] = 1;
+    return;
+  }
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = surv[i];
+    const uint32_t j = (uint32_t)(v >> 48);
+    const uint64_t b = v & ((1ull << 48) - 1);
+    const PJob J = jobs[j];
+    if (verify_dynamic(J.src, J.n, b)) atomicOr(&dbm[J.dbm + (b >> 5)], 1u << (b & 31));
+  }
 }
 
 __global__ void k_popc(const uint32_t* __restrict__ words, uint64_t count, uint32_t* __restrict__ out) {
@@ -529,20 +562,383 @@ __global__ void __launch_bounds__(ND_THREADS) k_decode_nodes(const PJob* __restr
     nodes[g] = nd;
     return;
   }
+  (void)T;  // dynamic nodes: k_dyn_scan (one warp per block)
+}
+
+
+// ---- warp-cooperative dynamic blocks -----------------------------------------
+// One warp per dynamic block.  Lane 0 parses the header; the block's bit range
+// (header end .. the next candidate, an estimate of the block end) is cut into
+// 32 chunks that the lanes decode at once from arbitrary bit offsets.  Huffman
+// decoding resynchronises quickly: each lane records its first REC symbol
+// starts, and the true decode entering a chunk (the previous lane's exit) is
+// advanced only until it lands on one of them.  Pass 2 (k_dyn_emit) then
+// decodes every lane's exact sub-range again, writing its output.
+constexpr int WD_WARPS = 4;
+constexpr int REC = 16;
+constexpr uint64_t NONE64 = ~0ull;
+
+struct LanePlan {
+  uint64_t begin, end;  // absolute bit positions of the lane's symbols [begin, end)
+  uint64_t out_off;     // output bytes before this lane (node-relative)
+  uint32_t m_off;       // matches before this lane (node-relative)
+  uint32_t pad;
+};
+
+struct DynExtra {
+  uint64_t static_begin;  // != NONE64: static blocks follow the dynamic one (lane 0 decodes them)
+  uint64_t dyn_out, dyn_nm;
+};
+
+struct WarpSm {
+  Tables T;
+  uint32_t rpos[32][REC];
+  uint32_t rout[32][REC];
+  uint32_t rnm[32][REC];
+};
+
+// one lit/len symbol (+ distance): 0 literal, 1 match, 2 end of block, -1 invalid
+__device__ __forceinline__ int dsym(BitReader& r, const Tables* T, const Lims& LL, const Lims& DL, uint32_t& len,
+                                    uint32_t& dist, uint32_t& lit) {
+  int sym = hdecode(r, &T->lit, LL);
+  if (sym < 0) return -1;
+  if (sym < 256) {
+    lit = (uint32_t)sym;
+    len = 1;
+    return 0;
+  }
+  if (sym == 256) return 2;
+  sym -= 257;
+  if (sym >= 29) return -1;
+  len = p_lbase[sym] + r.take(p_lext[sym]);
+  int ds = hdecode(r, &T->dist, DL);
+  if (ds < 0 || ds >= 30) return -1;
+  dist = p_dbase[ds] + r.take(p_dext[ds]);
+  if (r.past_end()) return -1;
+  return 1;
+}
+
+__global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restrict__ jobs,
+                                                           const uint32_t* __restrict__ node_job,
+                                                           const uint32_t* __restrict__ dyn_nodes, uint32_t ndyn_total,
+                                                           Node* __restrict__ nodes, Tables* __restrict__ tabs,
+                                                           LanePlan* __restrict__ plans, DynExtra* __restrict__ extra) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  WarpSm& W = reinterpret_cast<WarpSm*>(smraw)[threadIdx.x >> 5];
+  const uint32_t d = blockIdx.x * WD_WARPS + (threadIdx.x >> 5);
+  if (d >= ndyn_total) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t g = dyn_nodes[d];
+  const uint32_t jid = node_job[g];
+  const PJob J = jobs[jid];
+  Node nd = nodes[g];
+  // header (lane 0)
+  uint64_t d0 = 0;
+  int rc = 0;
+  bool final_blk = false;
+  if (lane == 0) {
+    BitReader r;
+    r.init(J.src, J.n, nd.start);
+    uint32_t hdr = r.take(3);
+    final_blk = hdr & 1;
+    rc = read_dynamic(r, &W.T);
+    d0 = r.pos;
+  }
+  rc = __shfl_sync(0xffffffffu, rc, 0);
+  d0 = __shfl_sync(0xffffffffu, d0, 0);
+  final_blk = __shfl_sync(0xffffffffu, (int)final_blk, 0);
+  if (rc) {
+    if (lane == 0) {
+      nd.flags = 8;  // dynamic, not ok
+      nodes[g] = nd;
+    }
+    return;
+  }
+  __syncwarp();
+  Lims LL, DL;
+  LL.load(&W.T.lit);
+  DL.load(&W.T.dist);
+  // estimated end: the next dynamic candidate of the same job
+  uint64_t E = 8 * J.n;
+  if (g + 1 < J.node0 + 1 + J.ndyn) E = min(E, nodes[g + 1].start);
+  if (E < d0 + 32 * 64) E = d0 + 32 * 64;
+  const uint64_t span = E - d0;
+  const uint64_t s_k = d0 + span * lane / 32, s_n = d0 + span * (lane + 1) / 32;
+  // round 1
   BitReader r;
-  r.init(J.src, J.n, nd.start);
-  uint32_t hdr = r.take(3);
-  bool final_seen = hdr & 1;
-  uint64_t out_len = 0;
-  uint32_t nmatch = 0;
-  int rc = read_dynamic(r, T);
-  if (!rc) rc = decode_codes<false>(r, T, out_len, nmatch, J.expected, nullptr, 0, nullptr, 0);
-  if (!rc && !final_seen) rc = decode_static_run(r, T, out_len, nmatch, J.expected, final_seen);
-  nd.end_bit = r.pos;
-  nd.out_len = out_len;
-  nd.nmatch = nmatch;
-  nd.flags = (rc == 0 ? 1 : 0) | (final_seen ? 2 : 0);
-  nodes[g] = nd;
+  r.init(J.src, J.n, s_k);
+  uint64_t out = 0, nm = 0;
+  int nrec = 0;
+  bool stuck = false;
+  uint64_t eob_at = NONE64, eob_end = 0, eob_out = 0, eob_nm = 0, err_at = NONE64;
+  while (r.pos < s_n) {
+    const uint64_t p = r.pos;
+    if (nrec < REC) {
+      W.rpos[lane][nrec] = (uint32_t)(p - d0);
+      W.rout[lane][nrec] = (uint32_t)out;
+      W.rnm[lane][nrec] = (uint32_t)nm;
+      nrec++;
+    }
+    uint32_t len = 0, dist = 0, lit = 0;
+    int t = dsym(r, &W.T, LL, DL, len, dist, lit);
+    if (t < 0) {
+      stuck = true;
+      err_at = p;
+      break;
+    }
+    if (t == 2) {
+      if (eob_at == NONE64) eob_at = p, eob_end = r.pos, eob_out = out, eob_nm = nm;
+      continue;
+    }
+    out += len;
+    nm += (t == 1);
+  }
+  const uint64_t f = stuck ? NONE64 : r.pos;
+  __syncwarp();
+  // fix-up rounds: the true decode enters lane k's chunk at F_{k-1}
+  uint64_t F = f, cnt_out = out, cnt_nm = nm;       // corrected results (lane 0 is exact)
+  // lane 0 decodes from the true block start: its events are real; others wait for the fix-up
+  uint64_t real_eob = lane == 0 ? eob_at : NONE64, real_eob_end = eob_end;
+  uint64_t real_err = lane == 0 ? err_at : NONE64;
+  uint64_t ev_out = eob_out, ev_nm = eob_nm;
+  uint64_t used = lane == 0 ? d0 : NONE64 - 1;
+  for (int iter = 0; iter < 33; iter++) {
+    uint64_t entry = __shfl_up_sync(0xffffffffu, F, 1);
+    bool blocked = __shfl_up_sync(0xffffffffu, (int)(real_eob != NONE64 || real_err != NONE64), 1);
+    if (lane == 0) entry = d0, blocked = false;
+    const bool redo = lane > 0 && entry != used && entry != NONE64 && !blocked;
+    if (!__any_sync(0xffffffffu, redo)) break;
+    if (redo) {
+      used = entry;
+      uint64_t t = entry, o = 0, m = 0;
+      int j = 0;
+      bool done = false;
+      real_eob = NONE64;
+      real_err = NONE64;
+      BitReader q;
+      q.init(J.src, J.n, t);
+      while (t < s_n) {
+        while (j < nrec && (uint64_t)W.rpos[lane][j] + d0 < t) j++;
+        if (j < nrec && (uint64_t)W.rpos[lane][j] + d0 == t) {
+          // synchronised with round 1 from record j on
+          const uint64_t base_o = W.rout[lane][j], base_m = W.rnm[lane][j];
+          if (eob_at != NONE64 && eob_at >= t && (err_at == NONE64 || eob_at < err_at)) {
+            real_eob = eob_at;
+            real_eob_end = eob_end;
+            ev_out = o + eob_out - base_o;
+            ev_nm = m + eob_nm - base_m;
+          } else if (err_at != NONE64 && err_at >= t) {
+            real_err = err_at;
+          }
+          cnt_out = o + out - base_o;
+          cnt_nm = m + nm - base_m;
+          F = f;
+          done = true;
+          break;
+        }
+        uint32_t len = 0, dist = 0, lit = 0;
+        const uint64_t p = t;
+        int ty = dsym(q, &W.T, LL, DL, len, dist, lit);
+        if (ty < 0) {
+          real_err = p;
+          done = true;
+          break;
+        }
+        if (ty == 2) {
+          real_eob = p;
+          real_eob_end = q.pos;
+          ev_out = o;
+          ev_nm = m;
+          cnt_out = o;
+          cnt_nm = m;
+          F = q.pos;
+          done = true;
+          break;
+        }
+        o += len;
+        m += (ty == 1);
+        t = q.pos;
+      }
+      if (!done) {
+        F = t;
+        cnt_out = o;
+        cnt_nm = m;
+      }
+    }
+  }
+  // the first lane whose true range holds an end-of-block (or an error) ends the block
+  const bool ev = real_eob != NONE64 || real_err != NONE64;
+  const unsigned evm = __ballot_sync(0xffffffffu, ev);
+  int kstar = evm ? __ffs(evm) - 1 : 31;
+  uint64_t lane_out = lane < kstar ? cnt_out : (lane == kstar && ev ? ev_out : (lane == kstar ? cnt_out : 0));
+  uint64_t lane_nm = lane < kstar ? cnt_nm : (lane == kstar && ev ? ev_nm : (lane == kstar ? cnt_nm : 0));
+  bool bad = lane == kstar && real_err != NONE64 && (real_eob == NONE64 || real_err < real_eob);
+  // no end-of-block inside the estimate: the last lane keeps decoding
+  uint64_t tail_end = 0;
+  if (!evm && lane == 31) {
+    BitReader q;
+    q.init(J.src, J.n, F);
+    for (;;) {
+      uint32_t len = 0, dist = 0, lit = 0;
+      const uint64_t p = q.pos;
+      int ty = dsym(q, &W.T, LL, DL, len, dist, lit);
+      if (ty < 0) {
+        bad = true;
+        break;
+      }
+      if (ty == 2) {
+        real_eob = p;
+        real_eob_end = q.pos;
+        break;
+      }
+      lane_out += len;
+      lane_nm += (ty == 1);
+      if (lane_out > J.expected) {
+        bad = true;
+        break;
+      }
+    }
+    tail_end = real_eob;
+  }
+  // prefix sums over lanes
+  uint64_t xo = lane_out, xm = lane_nm;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t a = __shfl_up_sync(0xffffffffu, xo, o), b = __shfl_up_sync(0xffffffffu, xm, o);
+    if (lane >= o) xo += a, xm += b;
+  }
+  const uint64_t tot_o = __shfl_sync(0xffffffffu, xo, 31), tot_m = __shfl_sync(0xffffffffu, xm, 31);
+  const bool anybad = __any_sync(0xffffffffu, bad);
+  // lane ranges for pass 2
+  const uint64_t begin = lane == 0 ? d0 : __shfl_up_sync(0xffffffffu, F, 1);
+  uint64_t end = lane < kstar ? F : (lane == kstar ? (evm ? real_eob : tail_end) : begin);
+  if (lane > kstar) end = begin;
+  LanePlan lp;
+  lp.begin = lane <= kstar ? begin : 0;
+  lp.end = lane <= kstar ? end : 0;
+  lp.out_off = xo - lane_out;
+  lp.m_off = (uint32_t)(xm - lane_nm);
+  lp.pad = 0;
+  plans[(uint64_t)d * 32 + lane] = lp;
+  const uint64_t blk_end = __shfl_sync(0xffffffffu, real_eob_end, kstar);
+  // copy the tables for pass 2
+  {
+    const uint32_t* srcw = reinterpret_cast<const uint32_t*>(&W.T);
+    uint32_t* dstw = reinterpret_cast<uint32_t*>(tabs + d);
+    for (uint32_t i = lane; i < sizeof(Tables) / 4; i += 32) dstw[i] = srcw[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    uint64_t out_len = tot_o, nmatch = tot_m;
+    bool ok = !anybad && out_len <= J.expected;
+    bool fin = final_blk;
+    uint64_t e_bit = blk_end;
+    DynExtra ex{NONE64, tot_o, tot_m};
+    if (ok && !fin) {
+      BitReader q;
+      q.init(J.src, J.n, blk_end);
+      q.refill();
+      if (((q.peek(3) >> 1) & 3) == 1) {
+        ex.static_begin = blk_end;
+        uint32_t nm32 = 0;
+        bool fs = false;
+        if (decode_static_run(q, &W.T, out_len, nm32, J.expected, fs)) ok = false;
+        nmatch += nm32;
+        fin = fs;
+        e_bit = q.pos;
+      }
+    }
+    extra[d] = ex;
+    nd.end_bit = e_bit;
+    nd.out_len = out_len;
+    nd.nmatch = (uint32_t)nmatch;
+    nd.flags = 8 | (ok ? 1 : 0) | (fin ? 2 : 0);
+    nodes[g] = nd;
+  }
+}
+
+__global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restrict__ jobs, const Chain* __restrict__ chains,
+                                                           const uint32_t* __restrict__ chain_nodes,
+                                                           const uint32_t* __restrict__ job_of_chain_block,
+                                                           const uint32_t* __restrict__ chain_block_base,
+                                                           const Node* __restrict__ nodes,
+                                                           const uint64_t* __restrict__ out_off,
+                                                           const uint64_t* __restrict__ m_off,
+                                                           const Tables* __restrict__ tabs,
+                                                           const LanePlan* __restrict__ plans,
+                                                           const DynExtra* __restrict__ extra,
+                                                           Match* __restrict__ matches, uint32_t* __restrict__ fail) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  Tables& T = reinterpret_cast<Tables*>(smraw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const uint32_t j = job_of_chain_block[blockIdx.x];
+  const PJob J = jobs[j];
+  const uint32_t i = (blockIdx.x - chain_block_base[j]) * WD_WARPS + (threadIdx.x >> 5);
+  if (i >= chains[j].len) return;
+  const uint32_t g = chain_nodes[J.node0 + i];
+  const Node nd = nodes[g];
+  if (!(nd.flags & 8)) return;
+  const uint32_t d = J.dyn_base + (g - J.node0 - 1);
+  {
+    const uint32_t* srcw = reinterpret_cast<const uint32_t*>(tabs + d);
+    uint32_t* dstw = reinterpret_cast<uint32_t*>(&T);
+    for (uint32_t k = lane; k < sizeof(Tables) / 4; k += 32) dstw[k] = srcw[k];
+  }
+  __syncwarp();
+  const LanePlan lp = plans[(uint64_t)d * 32 + lane];
+  const uint64_t base = out_off[J.node0 + i];
+  Match* mm = matches + J.mbase + m_off[J.node0 + i];
+  Lims LL, DL;
+  LL.load(&T.lit);
+  DL.load(&T.dist);
+  bool bad = false;
+  if (lp.end > lp.begin) {
+    BitReader r;
+    r.init(J.src, J.n, lp.begin);
+    uint64_t o = base + lp.out_off;
+    uint32_t m = lp.m_off;
+    while (r.pos < lp.end) {
+      uint32_t len = 0, dist = 0, lit = 0;
+      int ty = dsym(r, &T, LL, DL, len, dist, lit);
+      if (ty == 0) {
+        J.dst[o++] = (uint8_t)lit;
+      } else if (ty == 1) {
+        if (dist > o) {
+          bad = true;
+          break;
+        }
+        mm[m++] = Match{(uint32_t)o, (uint16_t)dist, (uint16_t)len};
+        o += len;
+      } else {
+        bad = true;  // an end-of-block or invalid code inside the lane's range
+        break;
+      }
+    }
+    if (r.pos != lp.end) bad = true;
+  }
+  const DynExtra ex = extra[d];
+  __syncwarp();
+  if (lane == 0 && ex.static_begin != NONE64 && !bad) {
+    BitReader r;
+    r.init(J.src, J.n, ex.static_begin);
+    uint64_t got = 0;
+    uint32_t nmatch = 0;
+    bool final_seen = false;
+    while (!final_seen) {
+      r.refill();
+      uint32_t h = r.peek(3);
+      if (((h >> 1) & 3) != 1) break;
+      r.drop(3);
+      static_tables(&T);
+      if (decode_codes<true>(r, &T, got, nmatch, nd.out_len - ex.dyn_out, J.dst, base + ex.dyn_out,
+                             mm + ex.dyn_nm, nd.nmatch - ex.dyn_nm)) {
+        bad = true;
+        break;
+      }
+      final_seen = h & 1;
+    }
+    if (ex.dyn_out + got != nd.out_len) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&fail[j], 1u);
 }
 
 // ---- P3 --------------------------------------------------------------------
@@ -590,12 +986,6 @@ __global__ void k_lift(const uint32_t* __restrict__ prev, uint32_t* __restrict__
   cur[g] = a >= SENT_END ? a : prev[a];
 }
 
-struct Chain {
-  uint32_t len;       // blocks on the chain (excluding the virtual start)
-  uint32_t terminal;  // SENT_END / SENT_BREAK / SENT_BAD
-  uint32_t last;      // last node (the virtual start if len == 0)
-  uint32_t pad;
-};
 
 __global__ void k_chain_len(const PJob* __restrict__ jobs, int njobs, const uint32_t* __restrict__ jump,
                             uint32_t nnodes, int levels, Chain* __restrict__ chains) {
@@ -686,6 +1076,7 @@ __global__ void __launch_bounds__(ND_THREADS) k_emit_nodes(const PJob* __restric
   if (i >= chains[j].len) return;
   const Node nd = nodes[chain_nodes[J.node0 + i]];
   if (nd.flags & 4) return;  // stored: copied by k_copy_stored
+  if (!(nd.flags & 8)) return;  // dynamic: k_dyn_emit (one warp per block)
   const uint64_t off = out_off[J.node0 + i];
   Match* mm = matches + J.mbase + m_off[J.node0 + i];
   BitReader r;
@@ -834,7 +1225,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
                                                               const uint32_t* __restrict__ fail,
                                                               const Match* __restrict__ matches,
                                                               ExtEntry* __restrict__ ext,
-                                                              uint32_t* __restrict__ ext_cnt) {
+                                                              uint32_t* __restrict__ ext_cnt,
+                                                              uint32_t* __restrict__ extp) {
   extern __shared__ uint32_t ent[];  // SUB entries: RESOLVED | value, or source relative to S - 65536
   __shared__ int changed;
   __shared__ uint32_t s_cnt;
@@ -878,33 +1270,38 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
     uint32_t e = ent[i];
     if (e & RESOLVED) {
       J.dst[S + i] = (uint8_t)e;
+      extp[J.xbase + S + i] = 0xFFFFFFFFu;
     } else {
       uint32_t k = atomicAdd(&s_cnt, 1u);
-      ext[(uint64_t)blockIdx.x * SUB + k] = ExtEntry{(uint32_t)(S + i), (uint32_t)(S + e - 65536)};
+      const uint32_t src = (uint32_t)(S + e - 65536);
+      ext[(uint64_t)blockIdx.x * SUB + k] = ExtEntry{(uint32_t)(S + i), src};
+      extp[J.xbase + S + i] = src;
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) ext_cnt[blockIdx.x] = s_cnt;
 }
 
-__global__ void __launch_bounds__(1024) k_resolve_ext(const PJob* __restrict__ jobs,
-                                                      const uint64_t* __restrict__ out_total,
+// Every byte left unresolved by its window points to an earlier byte; chase
+// the pointers (read-only map) to a byte its own window resolved.  Fully
+// parallel over all windows of all lanes.
+__global__ void __launch_bounds__(256) k_resolve_chase(const PJob* __restrict__ jobs,
+                                                      const uint32_t* __restrict__ job_of_sub,
                                                       const uint32_t* __restrict__ fail,
                                                       const ExtEntry* __restrict__ ext,
-                                                      const uint32_t* __restrict__ ext_cnt) {
-  const PJob J = jobs[blockIdx.x];
-  if (fail[blockIdx.x]) return;
-  const uint64_t total = out_total[2 * blockIdx.x];
-  const uint32_t nsub = (uint32_t)((total + SUB - 1) / SUB);
-  for (uint32_t s = 0; s < nsub; s++) {
-    const uint32_t g = J.sub0 + s;
-    const uint32_t c = ext_cnt[g];
-    const ExtEntry* E = ext + (uint64_t)g * SUB;
-    for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
-      ExtEntry e = E[k];
-      J.dst[e.dst] = J.dst[e.src];
-    }
-    __syncthreads();
+                                                      const uint32_t* __restrict__ ext_cnt,
+                                                      const uint32_t* __restrict__ extp) {
+  const uint32_t j = job_of_sub[blockIdx.x];
+  const PJob J = jobs[j];
+  if (fail[j]) return;
+  const uint32_t c = ext_cnt[blockIdx.x];
+  const ExtEntry* E = ext + (uint64_t)blockIdx.x * SUB;
+  const uint32_t* X = extp + J.xbase;
+  for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
+    const ExtEntry e = E[k];
+    uint32_t v = e.src, w;
+    while ((w = X[v]) != 0xFFFFFFFFu) v = w;
+    J.dst[e.dst] = J.dst[v];
   }
 }
 
@@ -1010,12 +1407,14 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_emit_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(WarpSm) * WD_WARPS)));
     attr = true;
   }
   std::vector<PJob> J(nj);
   std::vector<uint32_t> cand_job, sub_job, chunk_job, chunk_base(nj);
   std::vector<uint64_t> cand_byte0;
-  uint64_t dwords = 0, swords = 0, mtot = 0;
+  uint64_t dwords = 0, swords = 0, mtot = 0, xtot = 0, ntot_bytes = 0;
   uint32_t subs = 0;
   for (int i = 0; i < nj; i++) {
     PJob& p = J[i];
@@ -1031,6 +1430,9 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     p.mbase = mtot;
     p.mcap = p.expected / 3 + 1;
     mtot += p.mcap;
+    ntot_bytes += p.n;
+    p.xbase = xtot;
+    xtot += p.expected;
     p.sub0 = subs;
     p.nsub = (uint32_t)((p.expected + SUB - 1) / SUB);
     subs += p.nsub;
@@ -1046,7 +1448,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   size_t need = al(sizeof(PJob) * nj) + al(4 * cand_job.size()) + al(8 * cand_byte0.size()) + 2 * al(4 * dwords) +
                 2 * al(4 * swords) + al(4 * sub_job.size() + 4) + al(4 * chunk_job.size() + 4) + al(4 * nj) +
                 al(16 * chunk_job.size() + 16) + al(sizeof(Match) * mtot) + al(sizeof(ExtEntry) * (uint64_t)subs * SUB) +
-                al(4 * subs + 4) + al(4 * nj) * 6 + al(16 * nj) * 4 + al(sizeof(Chain) * nj) +
+                al(4 * subs + 4) + al(4 * xtot + 4) + al(8 * (ntot_bytes / 2 + 4096)) + 256 + al(4 * nj) * 6 + al(16 * nj) * 4 + al(sizeof(Chain) * nj) +
                 al(sizeof(Tables) * nj) + 65536;
   int rc = P->ws.reserve(need);
   if (rc) return rc;
@@ -1065,6 +1467,10 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   Match* d_matches = W.take<Match>(mtot);
   ExtEntry* d_ext = W.take<ExtEntry>((uint64_t)subs * SUB);
   uint32_t* d_ext_cnt = W.take<uint32_t>(subs + 1);
+  uint32_t* d_extp = W.take<uint32_t>(xtot + 1);
+  const uint64_t surv_cap = find_dynamic ? ntot_bytes / 2 + 4096 : 1;
+  uint64_t* d_surv = W.take<uint64_t>(surv_cap);
+  unsigned long long* d_surv_cnt = W.take<unsigned long long>(1);
   uint32_t* d_fail = W.take<uint32_t>(nj);
   uint32_t* d_want = W.take<uint32_t>(nj);
   uint64_t* d_totals = W.take<uint64_t>(2 * nj);
@@ -1085,9 +1491,14 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   BB_CUDA_TRY(cudaMemsetAsync(d_fail, 0, 4 * nj, st));
 
   // P1
+  BB_CUDA_TRY(cudaMemsetAsync(d_surv_cnt, 0, 8, st));
   k_candidates<<<(unsigned)cand_job.size(), 256, 0, st>>>(d_jobs, d_cand_job, d_cand_byte0, d_dbm, d_sbm,
-                                                          find_dynamic);
+                                                          find_dynamic, d_surv, d_surv_cnt, surv_cap);
   BB_LAUNCH_CHECK();
+  if (find_dynamic) {
+    k_verify_dynamic<<<kNumSMs * 8, 128, 0, st>>>(d_jobs, d_surv, d_surv_cnt, surv_cap, d_dbm, d_fail, nj);
+    BB_LAUNCH_CHECK();
+  }
   k_popc<<<grid_for(dwords, 256, 8), 256, 0, st>>>(d_dbm, dwords, d_dpre);
   BB_LAUNCH_CHECK();
   k_popc<<<grid_for(swords, 256, 8), 256, 0, st>>>(d_sbm, swords, d_spre);
@@ -1123,20 +1534,24 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i + 3, d_spre + send, 4, cudaMemcpyDeviceToHost, st));
   }
   BB_CUDA_TRY(cudaStreamSynchronize(st));
-  uint32_t nnodes = 0;
-  std::vector<uint32_t> node_job;
+  uint32_t nnodes = 0, ndyn_total = 0;
+  std::vector<uint32_t> node_job, dyn_nodes;
   for (int i = 0; i < nj; i++) {
     J[i].ndyn = P->h_pin[4 * i + 1] - P->h_pin[4 * i];
     J[i].nsto = P->h_pin[4 * i + 3] - P->h_pin[4 * i + 2];
     J[i].node0 = nnodes;
+    J[i].dyn_base = ndyn_total;
     uint32_t cnt = 1 + J[i].ndyn + 2 * J[i].nsto;
+    for (uint32_t k = 0; k < J[i].ndyn; k++) dyn_nodes.push_back(nnodes + 1 + k);
+    ndyn_total += J[i].ndyn;
     nnodes += cnt;
     node_job.insert(node_job.end(), cnt, (uint32_t)i);
   }
   int levels = 1;
   while ((1u << levels) <= nnodes + 1) levels++;
   size_t need2 = al(sizeof(Node) * nnodes) + al(4 * nnodes) + al(4ull * nnodes * levels) + al(4 * nnodes) +
-                 2 * al(8 * nnodes) + 4096;
+                 2 * al(8 * nnodes) + al(4ull * ndyn_total + 4) + al(sizeof(Tables) * (ndyn_total + 1)) +
+                 al(sizeof(LanePlan) * 32ull * (ndyn_total + 1)) + al(sizeof(DynExtra) * (ndyn_total + 1)) + 8192;
   Workspace& nodesw = P->nodesw;
   rc = nodesw.reserve(need2);
   if (rc) return rc;
@@ -1146,6 +1561,12 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   uint32_t* d_chain_nodes = nodesw.take<uint32_t>(nnodes);
   uint64_t* d_out_off = nodesw.take<uint64_t>(nnodes);
   uint64_t* d_m_off = nodesw.take<uint64_t>(nnodes);
+  uint32_t* d_dyn_nodes = nodesw.take<uint32_t>(ndyn_total + 1);
+  Tables* d_dtabs = nodesw.take<Tables>(ndyn_total + 1);
+  LanePlan* d_plans = nodesw.take<LanePlan>(32ull * (ndyn_total + 1));
+  DynExtra* d_extra = nodesw.take<DynExtra>(ndyn_total + 1);
+  if (ndyn_total)
+    BB_CUDA_TRY(cudaMemcpyAsync(d_dyn_nodes, dyn_nodes.data(), 4ull * ndyn_total, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_jobs, J.data(), sizeof(PJob) * nj, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_node_job, node_job.data(), 4 * nnodes, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemsetAsync(d_nodes, 0, sizeof(Node) * nnodes, st));
@@ -1159,6 +1580,11 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   k_decode_nodes<<<(nnodes + ND_THREADS - 1) / ND_THREADS, ND_THREADS, nd_smem, st>>>(d_jobs, d_node_job, nnodes,
                                                                                       d_nodes);
   BB_LAUNCH_CHECK();
+  if (ndyn_total) {
+    k_dyn_scan<<<(ndyn_total + WD_WARPS - 1) / WD_WARPS, 32 * WD_WARPS, sizeof(WarpSm) * WD_WARPS, st>>>(
+        d_jobs, d_node_job, d_dyn_nodes, ndyn_total, d_nodes, d_dtabs, d_plans, d_extra);
+    BB_LAUNCH_CHECK();
+  }
   T.mark("inflate.link_chain");
   // P3, P4
   k_link<<<(nnodes + 255) / 256, 256, 0, st>>>(d_jobs, d_node_job, nnodes, d_nodes, d_dbm, d_dpre, d_sbm, d_spre,
@@ -1187,7 +1613,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   std::vector<uint32_t> emit_job, emit_base(nj), copy_job, copy_base(nj);
   for (int i = 0; i < nj; i++) {
     emit_base[i] = (uint32_t)emit_job.size();
-    emit_job.insert(emit_job.end(), (hc[i].len + ND_THREADS - 1) / ND_THREADS, (uint32_t)i);
+    emit_job.insert(emit_job.end(), (hc[i].len + WD_WARPS - 1) / WD_WARPS, (uint32_t)i);
     copy_base[i] = (uint32_t)copy_job.size();
     copy_job.insert(copy_job.end(), hc[i].len, (uint32_t)i);
   }
@@ -1207,9 +1633,9 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   // P5
   T.mark("inflate.emit");
   if (!emit_job.empty()) {
-    k_emit_nodes<<<(unsigned)emit_job.size(), ND_THREADS, nd_smem, st>>>(d_jobs, nj, d_chains, d_chain_nodes,
-                                                                         d_emit_job, d_emit_base, d_nodes, d_out_off,
-                                                                         d_m_off, d_matches, d_fail);
+    k_dyn_emit<<<(unsigned)emit_job.size(), 32 * WD_WARPS, sizeof(Tables) * WD_WARPS, st>>>(
+        d_jobs, d_chains, d_chain_nodes, d_emit_job, d_emit_base, d_nodes, d_out_off, d_m_off, d_dtabs, d_plans,
+        d_extra, d_matches, d_fail);
     BB_LAUNCH_CHECK();
   }
   if (!copy_job.empty()) {
@@ -1224,9 +1650,9 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   T.mark("inflate.resolve");
   if (!sub_job.empty()) {
     k_resolve_local<<<(unsigned)sub_job.size(), RS_THREADS, SUB * 4, st>>>(d_jobs, d_sub_job, d_out_total, d_fail,
-                                                                     d_matches, d_ext, d_ext_cnt);
+                                                                     d_matches, d_ext, d_ext_cnt, d_extp);
     BB_LAUNCH_CHECK();
-    k_resolve_ext<<<nj, 1024, 0, st>>>(d_jobs, d_out_total, d_fail, d_ext, d_ext_cnt);
+    k_resolve_chase<<<(unsigned)sub_job.size(), 256, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp);
     BB_LAUNCH_CHECK();
   }
   // P7
