@@ -582,7 +582,8 @@ struct LanePlan {
   uint64_t begin, end;  // absolute bit positions of the lane's symbols [begin, end)
   uint64_t out_off;     // output bytes before this lane (node-relative)
   uint32_t m_off;       // matches before this lane (node-relative)
-  uint32_t pad;
+  uint32_t m_cnt;       // matches of this lane
+  uint64_t out_cnt;     // output bytes of this lane
 };
 
 struct DynExtra {
@@ -670,7 +671,9 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
   uint64_t out = 0, nm = 0;
   int nrec = 0;
   bool stuck = false;
+  // first two end-of-block symbols seen (a garbage one may precede the real one)
   uint64_t eob_at = NONE64, eob_end = 0, eob_out = 0, eob_nm = 0, err_at = NONE64;
+  uint64_t eob2_at = NONE64, eob2_end = 0, eob2_out = 0, eob2_nm = 0;
   while (r.pos < s_n) {
     const uint64_t p = r.pos;
     if (nrec < REC) {
@@ -688,6 +691,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
     }
     if (t == 2) {
       if (eob_at == NONE64) eob_at = p, eob_end = r.pos, eob_out = out, eob_nm = nm;
+      else if (eob2_at == NONE64) eob2_at = p, eob2_end = r.pos, eob2_out = out, eob2_nm = nm;
       continue;
     }
     out += len;
@@ -722,11 +726,15 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
         if (j < nrec && (uint64_t)W.rpos[lane][j] + d0 == t) {
           // synchronised with round 1 from record j on
           const uint64_t base_o = W.rout[lane][j], base_m = W.rnm[lane][j];
-          if (eob_at != NONE64 && eob_at >= t && (err_at == NONE64 || eob_at < err_at)) {
-            real_eob = eob_at;
-            real_eob_end = eob_end;
-            ev_out = o + eob_out - base_o;
-            ev_nm = m + eob_nm - base_m;
+          // the first end-of-block at or after the synchronisation point is real
+          uint64_t ea = eob_at, ee = eob_end, eo = eob_out, en = eob_nm;
+          if (ea != NONE64 && ea < t) ea = eob2_at, ee = eob2_end, eo = eob2_out, en = eob2_nm;
+          if (ea != NONE64 && ea < t) ea = NONE64;  // more than two: resolved by pass 2's checks
+          if (ea != NONE64 && (err_at == NONE64 || ea < err_at)) {
+            real_eob = ea;
+            real_eob_end = ee;
+            ev_out = o + eo - base_o;
+            ev_nm = m + en - base_m;
           } else if (err_at != NONE64 && err_at >= t) {
             real_err = err_at;
           }
@@ -817,7 +825,8 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
   lp.end = lane <= kstar ? end : 0;
   lp.out_off = xo - lane_out;
   lp.m_off = (uint32_t)(xm - lane_nm);
-  lp.pad = 0;
+  lp.m_cnt = lane <= kstar ? (uint32_t)lane_nm : 0;
+  lp.out_cnt = lane <= kstar ? lane_out : 0;
   plans[(uint64_t)d * 32 + lane] = lp;
   const uint64_t blk_end = __shfl_sync(0xffffffffu, real_eob_end, kstar);
   // copy the tables for pass 2
@@ -913,7 +922,9 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restri
         break;
       }
     }
-    if (r.pos != lp.end) bad = true;
+    if (r.pos != lp.end || o - (base + lp.out_off) != lp.out_cnt || m - lp.m_off != lp.m_cnt) bad = true;
+  } else if (lp.out_cnt || lp.m_cnt) {
+    bad = true;
   }
   const DynExtra ex = extra[d];
   __syncwarp();
@@ -1222,7 +1233,7 @@ struct ExtEntry {
 __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __restrict__ jobs,
                                                               const uint32_t* __restrict__ job_of_sub,
                                                               const uint64_t* __restrict__ out_total,
-                                                              const uint32_t* __restrict__ fail,
+                                                              uint32_t* __restrict__ fail,
                                                               const Match* __restrict__ matches,
                                                               ExtEntry* __restrict__ ext,
                                                               uint32_t* __restrict__ ext_cnt,
@@ -1245,16 +1256,32 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
   __syncthreads();
   // match bytes -> source pointers
   const uint64_t m0 = first_match_after(M, nm, S);
+  __shared__ int corrupt;
+  if (threadIdx.x == 0) corrupt = 0;
+  __syncthreads();
   for (uint64_t k = m0 + threadIdx.x; k < nm && M[k].dst < S + W; k += blockDim.x) {
     const Match mt = M[k];
+    if (mt.dist == 0 || mt.dist > mt.dst || mt.len < 3 || mt.len > 258) {
+      corrupt = 1;  // never produced by a valid decode: let the exact decoder take the job
+      continue;
+    }
     uint64_t a = max((uint64_t)mt.dst, S), b = min((uint64_t)mt.dst + mt.len, S + W);
     for (uint64_t x = a; x < b; x++) ent[x - S] = (uint32_t)(x - mt.dist - S + 65536);
   }
   __syncthreads();
-  // pointer jumping inside the window
+  if (corrupt) {
+    if (threadIdx.x == 0) atomicExch(&fail[j], 1u);
+    return;
+  }
+  // pointer jumping inside the window (every pointer goes strictly backwards)
+  int rounds = 0;
   do {
     __syncthreads();
     if (threadIdx.x == 0) changed = 0;
+    if (++rounds > 40) {
+      if (threadIdx.x == 0) atomicExch(&fail[j], 1u);
+      return;
+    }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) {
       uint32_t e = ent[i];
@@ -1287,7 +1314,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
 // parallel over all windows of all lanes.
 __global__ void __launch_bounds__(256) k_resolve_chase(const PJob* __restrict__ jobs,
                                                       const uint32_t* __restrict__ job_of_sub,
-                                                      const uint32_t* __restrict__ fail,
+                                                      uint32_t* __restrict__ fail,
                                                       const ExtEntry* __restrict__ ext,
                                                       const uint32_t* __restrict__ ext_cnt,
                                                       const uint32_t* __restrict__ extp) {
@@ -1300,7 +1327,13 @@ __global__ void __launch_bounds__(256) k_resolve_chase(const PJob* __restrict__ 
   for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
     const ExtEntry e = E[k];
     uint32_t v = e.src, w;
-    while ((w = X[v]) != 0xFFFFFFFFu) v = w;
+    while ((w = X[v]) != 0xFFFFFFFFu) {
+      if (w >= v) {  // sources always lie strictly earlier
+        atomicExch(&fail[j], 1u);
+        return;
+      }
+      v = w;
+    }
     J.dst[e.dst] = J.dst[v];
   }
 }
