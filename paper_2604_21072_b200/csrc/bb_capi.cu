@@ -10,6 +10,7 @@
 //   deflate decode guard src/codec.cpp:30-31 (expected > blob*1040 + 1024 -> CorruptContainer)
 //   identity decode      src/codec.cpp:45-47 (size mismatch -> CorruptContainer)
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -23,6 +24,15 @@ namespace bb {
 
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_stage_timing{0};
+
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BB_DEBUG_SYNC");
+    v = (e && *e == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 
 namespace {
 struct StageAcc {

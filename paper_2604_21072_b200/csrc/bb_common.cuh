@@ -25,9 +25,16 @@ constexpr int kNumSMs = 148;  // B200
     }                                                                                       \
   } while (0)
 
+bool debug_sync();  // BB_DEBUG_SYNC=1: synchronize + log after every launch
+
 #define BB_LAUNCH_CHECK()                                                                       \
   do {                                                                                          \
     bb::count_launch();                                                                         \
+    if (bb::debug_sync()) {                                                                     \
+      fprintf(stderr, "[bb] launch %s:%d\n", __FILE__, __LINE__);                              \
+      cudaDeviceSynchronize();                                                                  \
+      fprintf(stderr, "[bb]   done %s:%d\n", __FILE__, __LINE__);                              \
+    }                                                                                           \
     cudaError_t e_ = cudaGetLastError();                                                        \
     if (e_ != cudaSuccess) {                                                                    \
       bb::set_error("CUDA launch error %s at %s:%d", cudaGetErrorString(e_), __FILE__, __LINE__); \

@@ -29,6 +29,7 @@
 //   K7 k_emit         parallel bit packing of every block into the container
 //      k_adler*       Adler-32 (chunk sums + ordered combine), zlib header/trailer,
 //      k_finalize     BBC1 header
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -251,6 +252,77 @@ __global__ void __launch_bounds__(32) k_hash_prev(const LaneDev* __restrict__ la
     }
     wc = wn;
     xc = xn;
+  }
+}
+
+// K3 (sort-based): one CTA of 1024 threads per HP2_SEG positions with a
+// 32768-entry u32 head table in shared memory.  The 32 KiB history only needs
+// each hash's most recent position, so it is inserted order-free with
+// atomicMax.  Segment positions go 1024 at a time through a stable block radix
+// sort on the 15-bit hash: equal hashes become adjacent in position order, so a
+// position's predecessor is its sorted neighbour (or the head table), and the
+// last of each run updates the head.
+constexpr uint32_t HP2_SEG = 32768;
+constexpr int HP2_THREADS = 1024;
+
+__global__ void __launch_bounds__(HP2_THREADS, 1) k_hash_prev2(const LaneDev* __restrict__ lanes,
+                                                               const WorkItem* __restrict__ work,
+                                                               uint16_t* __restrict__ pd) {
+  typedef cub::BlockRadixSort<uint16_t, HP2_THREADS, 1, uint16_t> Sort;
+  extern __shared__ __align__(16) uint32_t hp2_smem[];
+  uint32_t* head = hp2_smem;  // 32768: position + 1 (0 = none)
+  __shared__ typename Sort::TempStorage sort_tmp;
+  __shared__ uint16_t s_key[HP2_THREADS];
+  __shared__ uint16_t s_val[HP2_THREADS];
+  __shared__ uint16_t s_out[HP2_THREADS];
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + HP2_SEG, n);
+  const uint64_t base = s > WSIZE ? s - WSIZE : 0;
+  const uint8_t* src = L.src;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 32768; i += HP2_THREADS) head[i] = 0;
+  __syncthreads();
+  // history: most recent position per hash (order-free)
+  for (uint64_t q = base + tid; q < s; q += HP2_THREADS) {
+    if (q + MIN_MATCH > n) continue;
+    uint32_t h = (((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^ __ldg(src + q + 2)) & 0x7fff;
+    atomicMax(&head[h], (uint32_t)(q - base + 1));
+  }
+  __syncthreads();
+  uint16_t* out = pd + L.pbase;
+  for (uint64_t c = s; c < e; c += HP2_THREADS) {
+    const uint64_t q = c + tid;
+    const bool valid = q < e && q + MIN_MATCH <= n;
+    uint16_t key[1], val[1];
+    key[0] = valid ? (uint16_t)((((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^
+                                 __ldg(src + q + 2)) & 0x7fff)
+                   : (uint16_t)0xffff;
+    val[0] = (uint16_t)tid;
+    Sort(sort_tmp).Sort(key, val, 0, 16);
+    // sorted order: thread i holds rank i
+    s_key[tid] = key[0];
+    s_val[tid] = val[0];
+    __syncthreads();
+    const uint16_t k = key[0], v = val[0];
+    uint32_t d = 0;
+    if (k != 0xffff) {
+      const uint64_t qq = c + v;
+      uint64_t pred = ~0ull;
+      if (tid > 0 && s_key[tid - 1] == k) {
+        pred = c + s_val[tid - 1];
+      } else if (head[k]) {
+        pred = base + head[k] - 1;
+      }
+      if (pred != ~0ull && qq - pred < WSIZE) d = (uint32_t)(qq - pred);
+    }
+    s_out[v] = (uint16_t)d;
+    __syncthreads();
+    if (k != 0xffff && (tid == HP2_THREADS - 1 || s_key[tid + 1] != k)) head[k] = (uint32_t)(c + v - base + 1);
+    if (q < e) out[q] = s_out[tid];
+    __syncthreads();
   }
 }
 
@@ -1405,7 +1477,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   if (!e->tables_ready) {
     ZTables t = make_tables();
     BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
     e->tables_ready = true;
   }
@@ -1450,7 +1522,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     d.slot = j.slot;
     if (j.slot == 0) C[j.container].lane0 = i;
     L[i] = d;
-    for (uint64_t s = 0; s < j.n; s += HP_SEG) hp_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
+    for (uint64_t s = 0; s < j.n; s += HP2_SEG) hp_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
     for (uint64_t s = 0; s < j.n; s += PF_SEG) pf_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
     ad_chunk0[i] = (uint32_t)ad_work.size();
     for (uint64_t s = 0; s * AD_CHUNK < j.n; s++) ad_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
@@ -1534,7 +1606,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   // K3, K4
   T.mark("deflate.hash_prev");
   if (!hp_work.empty()) {
-    k_hash_prev<<<(unsigned)hp_work.size(), 32, 65536, st>>>(d_lanes, d_hp, d_pd);
+    k_hash_prev2<<<(unsigned)hp_work.size(), HP2_THREADS, 131072, st>>>(d_lanes, d_hp, d_pd);
     BB_LAUNCH_CHECK();
   }
   T.mark("deflate.profile");
@@ -1641,13 +1713,13 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ZTables t = make_tables();
   BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
-  BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
   LaneDev d{};
   d.src = d_in;
   d.n = n;
   std::vector<WorkItem> hp, pf;
-  for (uint64_t s = 0; s < n; s += HP_SEG) hp.push_back(WorkItem{0, (uint32_t)s});
+  for (uint64_t s = 0; s < n; s += HP2_SEG) hp.push_back(WorkItem{0, (uint32_t)s});
   for (uint64_t s = 0; s < n; s += PF_SEG) pf.push_back(WorkItem{0, (uint32_t)s});
   LaneDev* dl;
   WorkItem *dh, *dp;
@@ -1658,7 +1730,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   if (!hp.empty()) BB_CUDA_TRY(cudaMemcpy(dh, hp.data(), sizeof(WorkItem) * hp.size(), cudaMemcpyHostToDevice));
   if (!pf.empty()) BB_CUDA_TRY(cudaMemcpy(dp, pf.data(), sizeof(WorkItem) * pf.size(), cudaMemcpyHostToDevice));
   if (!hp.empty()) {
-    k_hash_prev<<<(unsigned)hp.size(), 32, 65536, st>>>(dl, dh, d_pd);
+    k_hash_prev2<<<(unsigned)hp.size(), HP2_THREADS, 131072, st>>>(dl, dh, d_pd);
     BB_LAUNCH_CHECK();
   }
   if (!pf.empty() && d_prof) {

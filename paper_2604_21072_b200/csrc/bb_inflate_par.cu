@@ -30,6 +30,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <unistd.h>
+
 #include <cstring>
 #include <vector>
 
@@ -295,7 +297,9 @@ __device__ int decode_codes(BitReader& r, const Tables* T, uint64_t& out_len, ui
   Lims LL, DL;
   LL.load(&T->lit);
   DL.load(&T->dist);
+  uint64_t guard = 0;
   for (;;) {
+    if (++guard > (1ull << 26)) return -1;
     int sym = hdecode(r, &T->lit, LL);
     if (sym < 0) return -1;
     if (sym < 256) {
@@ -575,6 +579,15 @@ __global__ void __launch_bounds__(ND_THREADS) k_decode_nodes(const PJob* __restr
 // advanced only until it lands on one of them.  Pass 2 (k_dyn_emit) then
 // decodes every lane's exact sub-range again, writing its output.
 constexpr int WD_WARPS = 4;
+__device__ unsigned long long g_wd[8];  // watchdog trips per loop site (debug)
+__device__ unsigned* g_prog;             // debug: progress words in mapped host memory (or null)
+#define PROG(d, lane, ph, x) \
+  if (g_prog) ((volatile unsigned*)g_prog)[(d) * 32 + (lane)] = ((ph) << 24) | ((unsigned)(x) & 0xffffff)
+#define WD_GUARD(site, it, limit, action)        \
+  if (++(it) > (limit)) {                        \
+    atomicAdd(&g_wd[site], 1ull);                \
+    action;                                      \
+  }
 constexpr int REC = 16;
 constexpr uint64_t NONE64 = ~0ull;
 
@@ -633,6 +646,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
   const uint32_t jid = node_job[g];
   const PJob J = jobs[jid];
   Node nd = nodes[g];
+  PROG(d, lane, 1, 0);
   // header (lane 0)
   uint64_t d0 = 0;
   int rc = 0;
@@ -674,7 +688,10 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
   // first two end-of-block symbols seen (a garbage one may precede the real one)
   uint64_t eob_at = NONE64, eob_end = 0, eob_out = 0, eob_nm = 0, err_at = NONE64;
   uint64_t eob2_at = NONE64, eob2_end = 0, eob2_out = 0, eob2_nm = 0;
+  uint64_t it0 = 0;
   while (r.pos < s_n) {
+    WD_GUARD(0, it0, (1ull << 16), { stuck = true; err_at = r.pos; break; })
+    PROG(d, lane, 2, it0);
     const uint64_t p = r.pos;
     if (nrec < REC) {
       W.rpos[lane][nrec] = (uint32_t)(p - d0);
@@ -706,7 +723,10 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
   uint64_t real_err = lane == 0 ? err_at : NONE64;
   uint64_t ev_out = eob_out, ev_nm = eob_nm;
   uint64_t used = lane == 0 ? d0 : NONE64 - 1;
+  if (lane == 0) atomicAdd(&g_wd[5], 1ull);  // dynamic blocks scanned
   for (int iter = 0; iter < 33; iter++) {
+    if (lane == 0) atomicAdd(&g_wd[6], 1ull);  // fix-up iterations
+    PROG(d, lane, 4, iter);
     uint64_t entry = __shfl_up_sync(0xffffffffu, F, 1);
     bool blocked = __shfl_up_sync(0xffffffffu, (int)(real_eob != NONE64 || real_err != NONE64), 1);
     if (lane == 0) entry = d0, blocked = false;
@@ -721,7 +741,10 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
       real_err = NONE64;
       BitReader q;
       q.init(J.src, J.n, t);
+      uint64_t it1 = 0;
       while (t < s_n) {
+        WD_GUARD(1, it1, (1ull << 16), { real_err = t; done = true; break; })
+        PROG(d, lane, 5, it1);
         while (j < nrec && (uint64_t)W.rpos[lane][j] + d0 < t) j++;
         if (j < nrec && (uint64_t)W.rpos[lane][j] + d0 == t) {
           // synchronised with round 1 from record j on
@@ -786,7 +809,10 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
   if (!evm && lane == 31) {
     BitReader q;
     q.init(J.src, J.n, F);
+    uint64_t it2 = 0;
     for (;;) {
+      WD_GUARD(2, it2, (1ull << 20), { bad = true; break; })
+      PROG(d, lane, 6, it2);
       uint32_t len = 0, dist = 0, lit = 0;
       const uint64_t p = q.pos;
       int ty = dsym(q, &W.T, LL, DL, len, dist, lit);
@@ -808,6 +834,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
     }
     tail_end = real_eob;
   }
+  PROG(d, lane, 7, 0);
   // prefix sums over lanes
   uint64_t xo = lane_out, xm = lane_nm;
   for (int o = 1; o < 32; o <<= 1) {
@@ -816,8 +843,11 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
   }
   const uint64_t tot_o = __shfl_sync(0xffffffffu, xo, 31), tot_m = __shfl_sync(0xffffffffu, xm, 31);
   const bool anybad = __any_sync(0xffffffffu, bad);
+  PROG(d, lane, 8, ((unsigned)ev << 23) | ((unsigned)stuck << 22) | ((unsigned)(real_eob_end != 0) << 21) |
+                        (unsigned)(F == NONE64 || F - d0 > 0x1fffffull ? 0x1fffffull : F - d0));
   // lane ranges for pass 2
-  const uint64_t begin = lane == 0 ? d0 : __shfl_up_sync(0xffffffffu, F, 1);
+  const uint64_t F_prev = __shfl_up_sync(0xffffffffu, F, 1);  // every lane must take part
+  const uint64_t begin = lane == 0 ? d0 : F_prev;
   uint64_t end = lane < kstar ? F : (lane == kstar ? (evm ? real_eob : tail_end) : begin);
   if (lane > kstar) end = begin;
   LanePlan lp;
@@ -846,7 +876,9 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
       BitReader q;
       q.init(J.src, J.n, blk_end);
       q.refill();
+      PROG(d, 0, 10, (unsigned)(blk_end - nd.start));
       if (((q.peek(3) >> 1) & 3) == 1) {
+        PROG(d, 0, 11, 0);
         ex.static_begin = blk_end;
         uint32_t nm32 = 0;
         bool fs = false;
@@ -857,6 +889,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
       }
     }
     extra[d] = ex;
+    PROG(d, 0, 9, 0);
     nd.end_bit = e_bit;
     nd.out_len = out_len;
     nd.nmatch = (uint32_t)nmatch;
@@ -905,7 +938,9 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restri
     r.init(J.src, J.n, lp.begin);
     uint64_t o = base + lp.out_off;
     uint32_t m = lp.m_off;
+    uint64_t it3 = 0;
     while (r.pos < lp.end) {
+      WD_GUARD(3, it3, (1ull << 20), { bad = true; break; })
       uint32_t len = 0, dist = 0, lit = 0;
       int ty = dsym(r, &T, LL, DL, len, dist, lit);
       if (ty == 0) {
@@ -1582,6 +1617,10 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   }
   int levels = 1;
   while ((1u << levels) <= nnodes + 1) levels++;
+  if (debug_sync())
+    for (int i = 0; i < nj; i++)
+      fprintf(stderr, "[bb] inflate job %d: n=%llu expected=%llu ndyn=%u nsto=%u find_dynamic=%d\n", i,
+              (unsigned long long)J[i].n, (unsigned long long)J[i].expected, J[i].ndyn, J[i].nsto, find_dynamic);
   size_t need2 = al(sizeof(Node) * nnodes) + al(4 * nnodes) + al(4ull * nnodes * levels) + al(4 * nnodes) +
                  2 * al(8 * nnodes) + al(4ull * ndyn_total + 4) + al(sizeof(Tables) * (ndyn_total + 1)) +
                  al(sizeof(LanePlan) * 32ull * (ndyn_total + 1)) + al(sizeof(DynExtra) * (ndyn_total + 1)) + 8192;
@@ -1613,9 +1652,27 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   k_decode_nodes<<<(nnodes + ND_THREADS - 1) / ND_THREADS, ND_THREADS, nd_smem, st>>>(d_jobs, d_node_job, nnodes,
                                                                                       d_nodes);
   BB_LAUNCH_CHECK();
+  unsigned* h_prog = nullptr;
+  if (debug_sync() && ndyn_total) {
+    cudaHostAlloc(reinterpret_cast<void**>(&h_prog), 4ull * 32 * ndyn_total, cudaHostAllocMapped);
+    memset(h_prog, 0, 4ull * 32 * ndyn_total);
+    unsigned* dp = nullptr;
+    cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), h_prog, 0);
+    cudaMemcpyToSymbol(g_prog, &dp, sizeof(dp));
+  }
   if (ndyn_total) {
     k_dyn_scan<<<(ndyn_total + WD_WARPS - 1) / WD_WARPS, 32 * WD_WARPS, sizeof(WarpSm) * WD_WARPS, st>>>(
         d_jobs, d_node_job, d_dyn_nodes, ndyn_total, d_nodes, d_dtabs, d_plans, d_extra);
+    for (int sec = 0; h_prog && sec < 6; sec++) {
+      if (cudaStreamQuery(st) == cudaSuccess) break;
+      usleep(1000000);
+      fprintf(stderr, "[bb] k_dyn_scan progress after %d s:\n", sec + 1);
+      for (uint32_t d = 0; d < ndyn_total; d++) {
+        fprintf(stderr, "  blk %u:", d);
+        for (int l = 0; l < 32; l++) fprintf(stderr, " %x", h_prog[d * 32 + l]);
+        fprintf(stderr, "\n");
+      }
+    }
     BB_LAUNCH_CHECK();
   }
   T.mark("inflate.link_chain");
@@ -1704,3 +1761,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
 }
 
 }  // namespace bb
+
+extern "C" BB_API void bb_debug_inflate_watchdog(unsigned long long* out8) {
+  cudaMemcpyFromSymbol(out8, bb::par::g_wd, sizeof(unsigned long long) * 8);
+}
