@@ -285,11 +285,14 @@ __global__ void __launch_bounds__(HP2_THREADS, 1) k_hash_prev2(const LaneDev* __
   const int tid = threadIdx.x;
   for (int i = tid; i < 32768; i += HP2_THREADS) head[i] = 0;
   __syncthreads();
-  // history: most recent position per hash (order-free)
-  for (uint64_t q = base + tid; q < s; q += HP2_THREADS) {
+  // history: most recent position per hash, scanned from the newest end so a
+  // hash already set by a later position needs no atomic (low-entropy lanes
+  // would otherwise serialise on a few hot buckets)
+  for (uint64_t off = tid; off < s - base; off += HP2_THREADS) {
+    const uint64_t q = s - 1 - off;
     if (q + MIN_MATCH > n) continue;
     uint32_t h = (((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^ __ldg(src + q + 2)) & 0x7fff;
-    atomicMax(&head[h], (uint32_t)(q - base + 1));
+    if (head[h] < (uint32_t)(q - base + 1)) atomicMax(&head[h], (uint32_t)(q - base + 1));
   }
   __syncthreads();
   uint16_t* out = pd + L.pbase;

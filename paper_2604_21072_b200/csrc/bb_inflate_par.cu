@@ -92,6 +92,17 @@ struct Match {
   uint16_t len;
 };
 
+// job owning flat index x, given prefix[0..nj] (prefix[0] = 0) of per-job counts
+__device__ __forceinline__ int find_job(const uint64_t* __restrict__ prefix, int nj, uint64_t x) {
+  int lo = 0, hi = nj - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 // ---- bit access -------------------------------------------------------------
 __device__ __forceinline__ uint64_t load_le64_slow(const uint8_t* p, uint64_t n, uint64_t byte) {
   uint64_t v = 0;
@@ -417,13 +428,13 @@ __device__ __forceinline__ bool dyn_header_quick(uint64_t w0, uint64_t w1, uint3
 // Survivors of the quick test are appended to a list (warp-aggregated) and
 // verified exactly by k_verify_dynamic with one thread each, so the rare long
 // verifications do not serialise whole warps.
-__global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __restrict__ job_of_block,
-                             const uint64_t* __restrict__ block_byte0, uint32_t* __restrict__ dbm,
+__global__ void k_candidates(const PJob* __restrict__ jobs, const uint64_t* __restrict__ blk_prefix, int njobs,
+                             uint32_t* __restrict__ dbm,
                              uint32_t* __restrict__ sbm, int find_dynamic, uint64_t* __restrict__ surv,
                              unsigned long long* __restrict__ surv_cnt, uint64_t surv_cap) {
-  const uint32_t j = job_of_block[blockIdx.x];
+  const uint32_t j = (uint32_t)find_job(blk_prefix, njobs, blockIdx.x);
   const PJob J = jobs[j];
-  const uint64_t B = block_byte0[blockIdx.x] + threadIdx.x;  // one stream byte per thread
+  const uint64_t B = (blockIdx.x - blk_prefix[j]) * 256ull + threadIdx.x;  // one stream byte per thread
   const int lane = threadIdx.x & 31;
   uint32_t dbits = 0;
   bool st = false;
@@ -432,10 +443,7 @@ __global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __re
       const uint64_t w0 = peek64(J.src, J.n, 8 * B), w1 = peek64(J.src, J.n, 8 * B + 64);
       for (uint32_t k = 0; k < 8; k++) {
         const uint64_t b = 8 * B + k;
-        if (b >= 16 && b + 17 <= 8 * J.n && dyn_header_quick(w0, w1, k)) {
-          unsigned long long slot = atomicAdd(surv_cnt, 1ull);
-          if (slot < surv_cap) surv[slot] = ((uint64_t)j << 48) | b;
-        }
+        if (b >= 16 && b + 17 <= 8 * J.n && dyn_header_quick(w0, w1, k)) dbits |= 1u << k;
       }
     }
     if (B >= 2 && B + 4 <= J.n) {
@@ -444,7 +452,22 @@ __global__ void k_candidates(const PJob* __restrict__ jobs, const uint32_t* __re
       st = len == (~nlen & 0xffff) && B + 4 + len <= J.n;
     }
   }
-  (void)dbits;
+  // survivors: one atomic per warp (warp-aggregated append)
+  {
+    const uint32_t cnt = __popc(dbits);
+    uint32_t pre = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+    unsigned long long base = 0;
+    if (lane == 0 && tot) base = atomicAdd(surv_cnt, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    uint64_t slot = base + pre - cnt;
+    for (uint32_t v = dbits; v; v &= v - 1, slot++)
+      if (slot < surv_cap) surv[slot] = ((uint64_t)j << 48) | (8 * B + (__ffs(v) - 1));
+  }
   unsigned ball = __ballot_sync(0xffffffffu, st);
   if (lane == 0 && B < J.n + 32) sbm[J.sbm + (B >> 5)] = ball;
 }
@@ -1468,7 +1491,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   const int nj = (int)jobs.size();
   if (!nj) return BB_OK;
   StageTimer T(st);
-  T.mark("inflate.candidates");
+  T.mark("inflate.setup");
   static bool attr = false;
   size_t nd_smem = sizeof(Tables) * ND_THREADS;
   if (!attr) {
@@ -1480,8 +1503,8 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     attr = true;
   }
   std::vector<PJob> J(nj);
-  std::vector<uint32_t> cand_job, sub_job, chunk_job, chunk_base(nj);
-  std::vector<uint64_t> cand_byte0;
+  std::vector<uint32_t> sub_job, chunk_job, chunk_base(nj);
+  std::vector<uint64_t> blk_prefix(nj + 1, 0);
   uint64_t dwords = 0, swords = 0, mtot = 0, xtot = 0, ntot_bytes = 0;
   uint32_t subs = 0;
   for (int i = 0; i < nj; i++) {
@@ -1505,15 +1528,13 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     p.nsub = (uint32_t)((p.expected + SUB - 1) / SUB);
     subs += p.nsub;
     for (uint32_t s = 0; s < p.nsub; s++) sub_job.push_back(i);
-    for (uint64_t b = 0; b < p.n; b += 256) {
-      cand_job.push_back(i);
-      cand_byte0.push_back(b);
-    }
+    blk_prefix[i + 1] = blk_prefix[i] + (p.n + 255) / 256;
     chunk_base[i] = (uint32_t)chunk_job.size();
     for (uint64_t c = 0; c * PA_CHUNK < p.expected; c++) chunk_job.push_back(i);
   }
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  size_t need = al(sizeof(PJob) * nj) + al(4 * cand_job.size()) + al(8 * cand_byte0.size()) + 2 * al(4 * dwords) +
+  const uint64_t cand_blocks = blk_prefix[nj];
+  size_t need = al(sizeof(PJob) * nj) + al(8 * (nj + 1)) + 2 * al(4 * dwords) +
                 2 * al(4 * swords) + al(4 * sub_job.size() + 4) + al(4 * chunk_job.size() + 4) + al(4 * nj) +
                 al(16 * chunk_job.size() + 16) + al(sizeof(Match) * mtot) + al(sizeof(ExtEntry) * (uint64_t)subs * SUB) +
                 al(4 * subs + 4) + al(4 * xtot + 4) + al(8 * (ntot_bytes / 2 + 4096)) + 256 + al(4 * nj) * 6 + al(16 * nj) * 4 + al(sizeof(Chain) * nj) +
@@ -1522,8 +1543,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   if (rc) return rc;
   Workspace& W = P->ws;
   PJob* d_jobs = W.take<PJob>(nj);
-  uint32_t* d_cand_job = W.take<uint32_t>(cand_job.size());
-  uint64_t* d_cand_byte0 = W.take<uint64_t>(cand_byte0.size());
+  uint64_t* d_blk_prefix = W.take<uint64_t>(nj + 1);
   uint32_t* d_dbm = W.take<uint32_t>(dwords);
   uint32_t* d_dpre = W.take<uint32_t>(dwords);
   uint32_t* d_sbm = W.take<uint32_t>(swords);
@@ -1547,26 +1567,29 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   Tables* d_tabs = W.take<Tables>(nj);
 
   BB_CUDA_TRY(cudaMemcpyAsync(d_jobs, J.data(), sizeof(PJob) * nj, cudaMemcpyHostToDevice, st));
-  BB_CUDA_TRY(cudaMemcpyAsync(d_cand_job, cand_job.data(), 4 * cand_job.size(), cudaMemcpyHostToDevice, st));
-  BB_CUDA_TRY(cudaMemcpyAsync(d_cand_byte0, cand_byte0.data(), 8 * cand_byte0.size(), cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_blk_prefix, blk_prefix.data(), 8 * (nj + 1), cudaMemcpyHostToDevice, st));
   if (!sub_job.empty())
     BB_CUDA_TRY(cudaMemcpyAsync(d_sub_job, sub_job.data(), 4 * sub_job.size(), cudaMemcpyHostToDevice, st));
   if (!chunk_job.empty())
     BB_CUDA_TRY(cudaMemcpyAsync(d_chunk_job, chunk_job.data(), 4 * chunk_job.size(), cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_chunk_base, chunk_base.data(), 4 * nj, cudaMemcpyHostToDevice, st));
-  BB_CUDA_TRY(cudaMemsetAsync(d_dbm, 0, 4 * dwords, st));
+  if (find_dynamic) BB_CUDA_TRY(cudaMemsetAsync(d_dbm, 0, 4 * dwords, st));
+  else BB_CUDA_TRY(cudaMemsetAsync(d_dbm, 0, 4 * dwords, st));  // (bitmap must read as empty)
   BB_CUDA_TRY(cudaMemsetAsync(d_sbm, 0, 4 * swords, st));
   BB_CUDA_TRY(cudaMemsetAsync(d_fail, 0, 4 * nj, st));
 
   // P1
   BB_CUDA_TRY(cudaMemsetAsync(d_surv_cnt, 0, 8, st));
-  k_candidates<<<(unsigned)cand_job.size(), 256, 0, st>>>(d_jobs, d_cand_job, d_cand_byte0, d_dbm, d_sbm,
+  T.mark(find_dynamic ? "inflate.candidates_dyn" : "inflate.candidates_stored");
+  k_candidates<<<(unsigned)cand_blocks, 256, 0, st>>>(d_jobs, d_blk_prefix, nj, d_dbm, d_sbm,
                                                           find_dynamic, d_surv, d_surv_cnt, surv_cap);
   BB_LAUNCH_CHECK();
   if (find_dynamic) {
+    T.mark("inflate.verify_headers");
     k_verify_dynamic<<<kNumSMs * 8, 128, 0, st>>>(d_jobs, d_surv, d_surv_cnt, surv_cap, d_dbm, d_fail, nj);
     BB_LAUNCH_CHECK();
   }
+  T.mark("inflate.rank_scan");
   k_popc<<<grid_for(dwords, 256, 8), 256, 0, st>>>(d_dbm, dwords, d_dpre);
   BB_LAUNCH_CHECK();
   k_popc<<<grid_for(swords, 256, 8), 256, 0, st>>>(d_sbm, swords, d_spre);
@@ -1639,6 +1662,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   DynExtra* d_extra = nodesw.take<DynExtra>(ndyn_total + 1);
   if (ndyn_total)
     BB_CUDA_TRY(cudaMemcpyAsync(d_dyn_nodes, dyn_nodes.data(), 4ull * ndyn_total, cudaMemcpyHostToDevice, st));
+  T.mark("inflate.node_setup");
   BB_CUDA_TRY(cudaMemcpyAsync(d_jobs, J.data(), sizeof(PJob) * nj, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_node_job, node_job.data(), 4 * nnodes, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemsetAsync(d_nodes, 0, sizeof(Node) * nnodes, st));
