@@ -30,9 +30,11 @@
 //      k_adler*       Adler-32 (chunk sums + ordered combine), zlib header/trailer,
 //      k_finalize     BBC1 header
 #include <cub/block/block_radix_sort.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -255,6 +257,112 @@ __global__ void __launch_bounds__(32) k_hash_prev(const LaneDev* __restrict__ la
   }
 }
 
+// K3 (warp scan): one warp per HP_SEG positions with a 64 KiB u16 head table
+// (three CTAs per SM).  History: scanned newest-first, a hash's first (= most
+// recent) occurrence claims its head.  Segment: scanned oldest-first, 32
+// positions per step; __match_any_sync orders same-hash lanes.  Bytes come in
+// 128-position register tiles prefetched one step ahead.
+__global__ void __launch_bounds__(32) k_hash_prev3(const LaneDev* __restrict__ lanes,
+                                                   const WorkItem* __restrict__ work, uint16_t* __restrict__ pd) {
+  extern __shared__ uint16_t hp3_head[];  // relative position + 1 (0 = none)
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + HP_SEG, n);
+  const uint64_t base = s > WSIZE ? s - WSIZE : 0;
+  const int lane = threadIdx.x;
+  uint16_t* head = hp3_head;
+  uint4* h4 = reinterpret_cast<uint4*>(head);
+  for (int i = lane; i < 32768 * 2 / 16; i += 32) h4[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  const uint8_t* src = L.src;
+  // history, newest first: the highest lane of a group claims an unset head
+  for (uint64_t top = s; top > base;) {
+    const uint64_t c = top > base + 32 ? top - 32 : base;
+    const uint64_t q = c + lane;
+    const bool valid = q < top && q + MIN_MATCH <= n;
+    uint32_t h = 0x10000u + lane;
+    if (valid) h = (((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^ __ldg(src + q + 2)) & 0x7fff;
+    const unsigned peers = __match_any_sync(0xffffffffu, h);
+    if (valid && (peers >> lane) == 1u && head[h] == 0) head[h] = (uint16_t)(q - base + 1);
+    __syncwarp();
+    top = c;
+  }
+  uint16_t* out = pd + L.pbase;
+  uint32_t wc, xc;
+  hp_load_tile(src, n, s, lane, wc, xc);
+  for (uint64_t c = s; c < e; c += 128) {
+    uint32_t wn = 0, xn = 0;
+    if (c + 128 < e) hp_load_tile(src, n, c + 128, lane, wn, xn);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t i = 32 * k + lane;
+      const uint64_t q = c + i;
+      const uint32_t b0 = hp_byte(wc, xc, i), b1 = hp_byte(wc, xc, i + 1), b2 = hp_byte(wc, xc, i + 2);
+      const bool valid = q < e && q + MIN_MATCH <= n;
+      const uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, h);
+      const unsigned lower = peers & ((1u << lane) - 1);
+      uint32_t d = 0;
+      if (valid) {
+        if (lower) {
+          d = lane - (31 - __clz(lower));
+        } else {
+          const uint32_t r = head[h];
+          if (r) {
+            const uint64_t dd = q - (base + r - 1);
+            d = dd < WSIZE ? (uint32_t)dd : 0;
+          }
+        }
+      }
+      __syncwarp();
+      if (valid && (peers >> lane) == 1u) head[h] = (uint16_t)(q - base + 1);
+      __syncwarp();
+      if (q < e) out[q] = (uint16_t)d;
+    }
+    wc = wn;
+    xc = xn;
+  }
+}
+
+// K3 (device-wide sort): every position of every lane gets the key
+// (lane << 16 | hash) -- or (lane << 16 | 0x8000) when fewer than 3 bytes
+// remain -- and one stable LSD radix sort (CUB onesweep) brings equal hashes of
+// a lane together in position order; the previous element of a run is the
+// previous same-hash position.  O(n) work, bandwidth-bound.
+__global__ void k_hash_keys(const LaneDev* __restrict__ lanes, int nlanes, const uint64_t* __restrict__ lp,
+                            uint64_t total, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nlanes - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (lp[mid] <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    const LaneDev& L = lanes[lo];
+    const uint64_t q = g - lp[lo];
+    uint32_t k = 0x8000;
+    if (q + MIN_MATCH <= L.n)
+      k = (((uint32_t)__ldg(L.src + q) << 10) ^ ((uint32_t)__ldg(L.src + q + 1) << 5) ^ __ldg(L.src + q + 2)) & 0x7fff;
+    keys[g] = ((uint32_t)lo << 16) | k;
+    vals[g] = (uint32_t)q;
+  }
+}
+
+__global__ void k_links(const LaneDev* __restrict__ lanes, uint64_t total, const uint32_t* __restrict__ keys,
+                        const uint32_t* __restrict__ vals, uint16_t* __restrict__ pd) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[g], q = vals[g];
+    uint32_t d = 0;
+    if (!(k & 0x8000) && g > 0 && keys[g - 1] == k) {
+      const uint32_t dd = q - vals[g - 1];
+      d = dd < WSIZE ? dd : 0;
+    }
+    pd[lanes[k >> 16].pbase + q] = (uint16_t)d;
+  }
+}
+
 // K3 (sort-based): one CTA of 1024 threads per HP2_SEG positions with a
 // 32768-entry u32 head table in shared memory.  The 32 KiB history only needs
 // each hash's most recent position, so it is inserted order-free with
@@ -362,7 +470,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile(const LaneDev* __rest
   const uint16_t* pdl = pd + L.pbase;
   for (uint32_t i = threadIdx.x; i < wlen; i += blockDim.x) {
     const uint64_t q = wlo + i;
-    uint32_t v = q < e ? pdl[q] : 0;
+    uint32_t v = 0xffff;
+    if (q < e) {
+      const uint32_t l = pdl[q];
+      v = l ? l : 0xffff;
+    }
     if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
     if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
     w32[i] = v;
@@ -372,55 +484,60 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile(const LaneDev* __rest
   for (uint64_t p = s + threadIdx.x; p < e; p += blockDim.x) {
     const uint32_t ip = (uint32_t)(p - wlo);
     const uint32_t wp = w32[ip];
-    const uint32_t d0 = wp & 0xffff;
+    const uint32_t d0 = wp & 0xffff;  // 0xffff = no earlier position with this hash
     uint2 res = make_uint2(0, 0);
-    if (p + MIN_MATCH <= n && d0 != 0 && d0 <= MAX_DIST && p != d0) {
+    if (p + MIN_MATCH <= n && d0 <= MAX_DIST && p != d0) {
       const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
       const uint32_t nice = min(NICE_LENGTH, la);
       const uint32_t maxl = min(MAX_MATCH, la);
       const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
-      const uint32_t lim_rel = limit > wlo ? (uint32_t)(limit - wlo) : 0;  // candidates need ic > lim_rel
-      const bool lim_any = limit >= wlo;  // lim_rel meaningful (else only ic >= 0 needed... see below)
+      // candidates continue while (window index) > lim_s; -1 when the limit lies before the window
+      const int lim_s = limit >= wlo ? (int)(limit - wlo) : -1;
       const uint32_t flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
-      const uint32_t s01 = wp >> 16;
-      uint32_t best = MIN_MATCH - 1, bestd = 0, cnt = 0, r32 = 0;
-      bool r32_set = false;
-      uint32_t se01 = w32[ip + best - 1] >> 16;
-      uint32_t ic = ip - d0;
-      for (;;) {
-        cnt++;
-        const uint32_t wc = w32[ic];
-        const uint32_t we = w32[ic + best - 1];
-        if ((wc >> 16) == s01 && (we >> 16) == se01) {
-          uint32_t len = 2;
-          while (len < maxl) {
-            uint32_t x = (w32[ic + len] ^ w32[ip + len]) >> 16;
-            if (x) {
-              len += (x & 0xff) == 0;
-              break;
-            }
-            len += 2;
-          }
-          len = min(len, maxl);
-          if (len > best) {
-            best = len;
-            bestd = ip - ic;
-            if (len >= nice) break;
-            se01 = w32[ip + best - 1] >> 16;
-          }
-        }
-        if (cnt == 32) {
-          r32 = prof_pack(best, bestd);
-          r32_set = true;
-        }
-        if (cnt == MAX_CHAIN) break;
-        const uint32_t dd = wc & 0xffff;
-        if (dd == 0 || dd > ic) break;
-        const uint32_t nx = ic - dd;
-        if (lim_any ? nx <= lim_rel : false) break;
-        ic = nx;
-      }
-      if (!r32_set) r32 = prof_pack(best, bestd);
+      const uint32_t s01 = wp & 0xffff0000u;
+      uint32_t best = MIN_MATCH - 1, bestd = 0, r32 = 0;
+      uint32_t se01 = w32[ip + best - 1] & 0xffff0000u;
+      int ic = (int)(ip - d0);
+      int cnt = 0;
+      bool stop = false;
+      // one chain step: quick reject on bytes (0,1) and (best-1,best), then extend
+#define PF_STEP()                                                                 \
+  {                                                                               \
+    const uint32_t wc = w32[ic];                                                  \
+    const uint32_t we = w32[ic + best - 1];                                       \
+    if ((((wc & 0xffff0000u) ^ s01) | ((we & 0xffff0000u) ^ se01)) == 0) {       \
+      uint32_t len = 2;                                                           \
+      while (len < maxl) {                                                        \
+        const uint32_t x = (w32[ic + len] ^ w32[ip + len]) >> 16;                 \
+        if (x) {                                                                  \
+          len += (x & 0xff) == 0;                                                 \
+          break;                                                                  \
+        }                                                                         \
+        len += 2;                                                                 \
+      }                                                                           \
+      len = min(len, maxl);                                                       \
+      if (len > best) {                                                           \
+        best = len;                                                               \
+        bestd = ip - (uint32_t)ic;                                                \
+        if (len >= nice) {                                                        \
+          stop = true;                                                            \
+          break;                                                                  \
+        }                                                                         \
+        se01 = w32[ip + best - 1] & 0xffff0000u;                                  \
+      }                                                                           \
+    }                                                                             \
+    const int nx = ic - (int)(wc & 0xffff);                                       \
+    if (nx <= lim_s) {                                                            \
+      stop = true;                                                                \
+      break;                                                                      \
+    }                                                                             \
+    ic = nx;                                                                      \
+  }
+      for (cnt = 1; cnt <= 32; cnt++) PF_STEP();
+      r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
+      if (!stop)
+        for (cnt = 33; cnt <= (int)MAX_CHAIN; cnt++) PF_STEP();
+#undef PF_STEP
       res.x = prof_pack(best, bestd) | flag;
       res.y = r32 | flag;
     }
@@ -1446,11 +1563,44 @@ __global__ void k_container_header(const ContainerDev* __restrict__ cons, int nc
 
 }  // namespace
 
+
+// K3 launcher (key generation, CUB onesweep radix sort, link scatter)
+static int hash_prev_sorted(Workspace& sortws, Workspace& W, const LaneDev* d_lanes, int nl,
+                            const std::vector<uint64_t>& lane_prefix, uint16_t* d_pd, cudaStream_t st) {
+  const uint64_t npos_exact = lane_prefix[nl];
+  int lane_bits = 1;
+  while ((1 << lane_bits) < nl) lane_bits++;
+  if (nl > 65535 || npos_exact >= (1ull << 31)) {
+    set_error("deflate: too many lanes/positions in one call");
+    return BB_ERROR;
+  }
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)npos_exact, 0, 16 + lane_bits, st);
+  int rc = sortws.reserve(16 * npos_exact + tmp_bytes + 4096);
+  if (rc) return rc;
+  uint32_t* k0 = sortws.take<uint32_t>(npos_exact);
+  uint32_t* k1 = sortws.take<uint32_t>(npos_exact);
+  uint32_t* v0 = sortws.take<uint32_t>(npos_exact);
+  uint32_t* v1 = sortws.take<uint32_t>(npos_exact);
+  void* tmp = sortws.take<uint8_t>(tmp_bytes);
+  uint64_t* d_lp = W.take<uint64_t>(nl + 1);
+  BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
+  k_hash_keys<<<grid_for(npos_exact, 256, 16), 256, 0, st>>>(d_lanes, nl, d_lp, npos_exact, k0, v0);
+  BB_LAUNCH_CHECK();
+  BB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int)npos_exact, 0, 16 + lane_bits, st));
+  count_launch(4);
+  k_links<<<grid_for(npos_exact, 256, 16), 256, 0, st>>>(d_lanes, npos_exact, k1, v1, d_pd);
+  BB_LAUNCH_CHECK();
+  return BB_OK;
+}
+
 // ---------------------------------------------------------------------------
 // host orchestration
 
 struct DeflateEngine {
   Workspace ws;
+  Workspace sortws;  // keys/values (x2) + CUB temp storage for K3
   bool tables_ready = false;
   uint64_t* h_pinned = nullptr;  // small pinned scratch for results
   size_t h_pinned_cap = 0;
@@ -1481,6 +1631,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     ZTables t = make_tables();
     BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
     e->tables_ready = true;
   }
@@ -1525,7 +1676,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     d.slot = j.slot;
     if (j.slot == 0) C[j.container].lane0 = i;
     L[i] = d;
-    for (uint64_t s = 0; s < j.n; s += HP2_SEG) hp_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
+    for (uint64_t s = 0; s < j.n; s += HP_SEG) hp_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
     for (uint64_t s = 0; s < j.n; s += PF_SEG) pf_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
     ad_chunk0[i] = (uint32_t)ad_work.size();
     for (uint64_t s = 0; s * AD_CHUNK < j.n; s++) ad_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
@@ -1538,6 +1689,9 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     maxG = std::max(maxG, d.G);
   }
   const uint32_t sym_stride = maxG + 1;
+  std::vector<uint64_t> lane_prefix(nl + 1, 0);
+  for (int i = 0; i < nl; i++) lane_prefix[i + 1] = lane_prefix[i] + L[i].n;
+  const uint64_t npos_exact = lane_prefix[nl];
   // workspace layout
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t need = 0;
@@ -1552,7 +1706,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   need += al(sizeof(LaneSyms) * nl) + al(sizeof(BlockInfo) * blk_total) + al(sizeof(BlockCodes) * blk_total);
   need += al(HDR_BYTES * (size_t)blk_total) + al(sizeof(BlockPlan) * blk_total);
   need += al(8 * nl) + al(sizeof(uint8_t*) * nl) + al(8 * nc) + al(4 * nc) + al(sizeof(Adl) * ad_work.size() + 16);
-  need += 64 * 256;
+  need += 64 * 256 + al(8 * (nl + 1));
   int rc = e->ws.reserve(need);
   if (rc) return rc;
   Workspace& W = e->ws;
@@ -1608,8 +1762,12 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
 
   // K3, K4
   T.mark("deflate.hash_prev");
-  if (!hp_work.empty()) {
-    k_hash_prev2<<<(unsigned)hp_work.size(), HP2_THREADS, 131072, st>>>(d_lanes, d_hp, d_pd);
+  static const int k3_sorted = getenv("BB_K3_SORT") ? 1 : 0;
+  if (npos_exact && k3_sorted) {
+    rc = hash_prev_sorted(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
+    if (rc) return rc;
+  } else if (!hp_work.empty()) {
+    k_hash_prev3<<<(unsigned)hp_work.size(), 32, 65536, st>>>(d_lanes, d_hp, d_pd);
     BB_LAUNCH_CHECK();
   }
   T.mark("deflate.profile");
@@ -1717,12 +1875,13 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   ZTables t = make_tables();
   BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
   LaneDev d{};
   d.src = d_in;
   d.n = n;
   std::vector<WorkItem> hp, pf;
-  for (uint64_t s = 0; s < n; s += HP2_SEG) hp.push_back(WorkItem{0, (uint32_t)s});
+  for (uint64_t s = 0; s < n; s += HP_SEG) hp.push_back(WorkItem{0, (uint32_t)s});
   for (uint64_t s = 0; s < n; s += PF_SEG) pf.push_back(WorkItem{0, (uint32_t)s});
   LaneDev* dl;
   WorkItem *dh, *dp;
@@ -1732,8 +1891,17 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   BB_CUDA_TRY(cudaMemcpy(dl, &d, sizeof d, cudaMemcpyHostToDevice));
   if (!hp.empty()) BB_CUDA_TRY(cudaMemcpy(dh, hp.data(), sizeof(WorkItem) * hp.size(), cudaMemcpyHostToDevice));
   if (!pf.empty()) BB_CUDA_TRY(cudaMemcpy(dp, pf.data(), sizeof(WorkItem) * pf.size(), cudaMemcpyHostToDevice));
-  if (!hp.empty()) {
-    k_hash_prev2<<<(unsigned)hp.size(), HP2_THREADS, 131072, st>>>(dl, dh, d_pd);
+  if (n && getenv("BB_K3_SORT")) {
+    Workspace sw, w2;
+    int rc = w2.reserve(4096);
+    if (rc) return rc;
+    std::vector<uint64_t> lp{0, n};
+    rc = hash_prev_sorted(sw, w2, dl, 1, lp, d_pd, st);
+    if (rc) return rc;
+    BB_CUDA_TRY(cudaStreamSynchronize(st));
+  } else if (!hp.empty()) {
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    k_hash_prev3<<<(unsigned)hp.size(), 32, 65536, st>>>(dl, dh, d_pd);
     BB_LAUNCH_CHECK();
   }
   if (!pf.empty() && d_prof) {
