@@ -1566,7 +1566,8 @@ __global__ void k_container_header(const ContainerDev* __restrict__ cons, int nc
 
 // K3 launcher (key generation, CUB onesweep radix sort, link scatter)
 static int hash_prev_sorted(Workspace& sortws, Workspace& W, const LaneDev* d_lanes, int nl,
-                            const std::vector<uint64_t>& lane_prefix, uint16_t* d_pd, cudaStream_t st) {
+                            const std::vector<uint64_t>& lane_prefix, uint16_t* d_pd, cudaStream_t st,
+                            StageTimer* T = nullptr) {
   const uint64_t npos_exact = lane_prefix[nl];
   int lane_bits = 1;
   while ((1 << lane_bits) < nl) lane_bits++;
@@ -1586,10 +1587,13 @@ static int hash_prev_sorted(Workspace& sortws, Workspace& W, const LaneDev* d_la
   void* tmp = sortws.take<uint8_t>(tmp_bytes);
   uint64_t* d_lp = W.take<uint64_t>(nl + 1);
   BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
+  if (T) T->mark("deflate.k3_keys");
   k_hash_keys<<<grid_for(npos_exact, 256, 16), 256, 0, st>>>(d_lanes, nl, d_lp, npos_exact, k0, v0);
   BB_LAUNCH_CHECK();
+  if (T) T->mark("deflate.k3_sort");
   BB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int)npos_exact, 0, 16 + lane_bits, st));
   count_launch(4);
+  if (T) T->mark("deflate.k3_links");
   k_links<<<grid_for(npos_exact, 256, 16), 256, 0, st>>>(d_lanes, npos_exact, k1, v1, d_pd);
   BB_LAUNCH_CHECK();
   return BB_OK;
@@ -1764,7 +1768,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   T.mark("deflate.hash_prev");
   static const int k3_sorted = getenv("BB_K3_SORT") ? 1 : 0;
   if (npos_exact && k3_sorted) {
-    rc = hash_prev_sorted(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
+    rc = hash_prev_sorted(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st, &T);
     if (rc) return rc;
   } else if (!hp_work.empty()) {
     k_hash_prev3<<<(unsigned)hp_work.size(), 32, 65536, st>>>(d_lanes, d_hp, d_pd);

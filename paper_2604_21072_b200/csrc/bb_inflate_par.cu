@@ -1182,7 +1182,19 @@ __global__ void k_copy_stored(const PJob* __restrict__ jobs, const Chain* __rest
   if (!(nd.flags & 4)) return;
   const uint8_t* s = J.src + nd.start + 4;
   uint8_t* d = J.dst + out_off[J.node0 + i];
-  for (uint64_t k = threadIdx.x; k < nd.out_len; k += blockDim.x) d[k] = s[k];
+  const uint64_t len = nd.out_len;
+  // aligned 16-byte output words, sources gathered with aligned loads
+  const uintptr_t da = reinterpret_cast<uintptr_t>(d);
+  const uint64_t head0 = (16 - (da & 15)) & 15;
+  const uint64_t head = head0 < len ? head0 : len;
+  const uint64_t words = (len - head) / 16;
+  for (uint64_t w = threadIdx.x; w < words; w += blockDim.x) {
+    uint32_t v[4];
+    gather16(s + head + 16 * w, v);
+    *reinterpret_cast<uint4*>(d + head + 16 * w) = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  for (uint64_t k = threadIdx.x; k < head; k += blockDim.x) d[k] = s[k];
+  for (uint64_t k = head + 16 * words + threadIdx.x; k < len; k += blockDim.x) d[k] = s[k];
 }
 
 // Sequential continuation after a BREAK (static block not covered by a node) and
@@ -1295,7 +1307,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
                                                               const Match* __restrict__ matches,
                                                               ExtEntry* __restrict__ ext,
                                                               uint32_t* __restrict__ ext_cnt,
-                                                              uint32_t* __restrict__ extp) {
+                                                              uint32_t* __restrict__ extp,
+                                                              uint8_t* __restrict__ wflag) {
   extern __shared__ uint32_t ent[];  // SUB entries: RESOLVED | value, or source relative to S - 65536
   __shared__ int changed;
   __shared__ uint32_t s_cnt;
@@ -1309,11 +1322,19 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
   const uint32_t W = (uint32_t)min((uint64_t)SUB, total - S);
   const uint64_t nm = out_total[2 * j + 1];
   const Match* M = matches + J.mbase;
+  // match bytes -> source pointers
+  const uint64_t m0 = first_match_after(M, nm, S);
+  if (m0 >= nm || M[m0].dst >= S + W) {  // no match reaches this window: bytes are final
+    if (threadIdx.x == 0) {
+      wflag[blockIdx.x] = 0;
+      ext_cnt[blockIdx.x] = 0;
+    }
+    return;
+  }
+  if (threadIdx.x == 0) wflag[blockIdx.x] = 1;
   for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) ent[i] = RESOLVED | J.dst[S + i];
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
-  // match bytes -> source pointers
-  const uint64_t m0 = first_match_after(M, nm, S);
   __shared__ int corrupt;
   if (threadIdx.x == 0) corrupt = 0;
   __syncthreads();
@@ -1375,17 +1396,21 @@ __global__ void __launch_bounds__(256) k_resolve_chase(const PJob* __restrict__ 
                                                       uint32_t* __restrict__ fail,
                                                       const ExtEntry* __restrict__ ext,
                                                       const uint32_t* __restrict__ ext_cnt,
-                                                      const uint32_t* __restrict__ extp) {
+                                                      const uint32_t* __restrict__ extp,
+                                                      const uint8_t* __restrict__ wflag) {
   const uint32_t j = job_of_sub[blockIdx.x];
   const PJob J = jobs[j];
   if (fail[j]) return;
+  const uint64_t S0 = (uint64_t)(blockIdx.x - J.sub0) * SUB;
+  (void)S0;
   const uint32_t c = ext_cnt[blockIdx.x];
   const ExtEntry* E = ext + (uint64_t)blockIdx.x * SUB;
   const uint32_t* X = extp + J.xbase;
   for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
     const ExtEntry e = E[k];
+    const uint8_t* WF = wflag + J.sub0;
     uint32_t v = e.src, w;
-    while ((w = X[v]) != 0xFFFFFFFFu) {
+    while (WF[v / SUB] && (w = X[v]) != 0xFFFFFFFFu) {
       if (w >= v) {  // sources always lie strictly earlier
         atomicExch(&fail[j], 1u);
         return;
@@ -1413,7 +1438,17 @@ __global__ void __launch_bounds__(PA_THREADS) k_adler_part(const PJob* __restric
   const uint64_t c0 = min(c * PA_CHUNK + threadIdx.x * per, J.expected);
   const uint64_t c1 = min(c0 + per, min((c + 1) * PA_CHUNK, J.expected));
   uint64_t A = 0, B = 0;
-  for (uint64_t i = c0; i < c1; i++) {
+  uint64_t i = c0;
+  for (; i + 16 <= c1; i += 16) {
+    uint32_t v[4];
+    gather16(J.dst + i, v);
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      A += (v[k >> 2] >> (8 * (k & 3))) & 0xff;
+      B += A;
+    }
+  }
+  for (; i < c1; i++) {
     A += J.dst[i];
     B += A;
   }
@@ -1537,7 +1572,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   size_t need = al(sizeof(PJob) * nj) + al(8 * (nj + 1)) + 2 * al(4 * dwords) +
                 2 * al(4 * swords) + al(4 * sub_job.size() + 4) + al(4 * chunk_job.size() + 4) + al(4 * nj) +
                 al(16 * chunk_job.size() + 16) + al(sizeof(Match) * mtot) + al(sizeof(ExtEntry) * (uint64_t)subs * SUB) +
-                al(4 * subs + 4) + al(4 * xtot + 4) + al(8 * (ntot_bytes / 2 + 4096)) + 256 + al(4 * nj) * 6 + al(16 * nj) * 4 + al(sizeof(Chain) * nj) +
+                al(4 * subs + 4) + al(subs + 4) + al(4 * xtot + 4) + al(8 * (ntot_bytes / 2 + 4096)) + 256 + al(4 * nj) * 6 + al(16 * nj) * 4 + al(sizeof(Chain) * nj) +
                 al(sizeof(Tables) * nj) + 65536;
   int rc = P->ws.reserve(need);
   if (rc) return rc;
@@ -1556,6 +1591,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   ExtEntry* d_ext = W.take<ExtEntry>((uint64_t)subs * SUB);
   uint32_t* d_ext_cnt = W.take<uint32_t>(subs + 1);
   uint32_t* d_extp = W.take<uint32_t>(xtot + 1);
+  uint8_t* d_wflag = W.take<uint8_t>(subs + 1);
   const uint64_t surv_cap = find_dynamic ? ntot_bytes / 2 + 4096 : 1;
   uint64_t* d_surv = W.take<uint64_t>(surv_cap);
   unsigned long long* d_surv_cnt = W.take<unsigned long long>(1);
@@ -1764,9 +1800,10 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   T.mark("inflate.resolve");
   if (!sub_job.empty()) {
     k_resolve_local<<<(unsigned)sub_job.size(), RS_THREADS, SUB * 4, st>>>(d_jobs, d_sub_job, d_out_total, d_fail,
-                                                                     d_matches, d_ext, d_ext_cnt, d_extp);
+                                                                     d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
     BB_LAUNCH_CHECK();
-    k_resolve_chase<<<(unsigned)sub_job.size(), 256, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp);
+    k_resolve_chase<<<(unsigned)sub_job.size(), 256, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
+                                                             d_wflag);
     BB_LAUNCH_CHECK();
   }
   // P7
