@@ -326,6 +326,124 @@ __global__ void __launch_bounds__(32) k_hash_prev3(const LaneDev* __restrict__ l
   }
 }
 
+// K3 (two-phase warp scan, current): the segments are independent.
+//   k_hash_prev4: one warp per 32 Ki-position segment scans it in order with an
+//     empty 64 KiB u16 head table; positions whose hash has not yet been seen in
+//     the segment get 0xffff ("look in the previous segment"), and the final
+//     table (last occurrence of every hash in the segment) is stored.
+//   k_hash_fix: those positions read the previous segment's table.
+// No history pass: each position is scanned once.
+constexpr uint32_t HP4_SEG = 32768;
+
+__global__ void __launch_bounds__(32) k_hash_prev4(const LaneDev* __restrict__ lanes,
+                                                   const WorkItem* __restrict__ work, uint16_t* __restrict__ pd,
+                                                   uint16_t* __restrict__ seg_heads) {
+  extern __shared__ uint16_t hp4_head[];  // position - s + 1 (0 = none)
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + HP4_SEG, n);
+  const int lane = threadIdx.x;
+  uint16_t* head = hp4_head;
+  uint4* h4 = reinterpret_cast<uint4*>(head);
+  for (int i = lane; i < 32768 * 2 / 16; i += 32) h4[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  const uint8_t* src = L.src;
+  uint16_t* out = pd + L.pbase;
+  uint32_t wc, xc;
+  hp_load_tile(src, n, s, lane, wc, xc);
+  for (uint64_t c = s; c < e; c += 128) {
+    uint32_t wn = 0, xn = 0;
+    if (c + 128 < e) hp_load_tile(src, n, c + 128, lane, wn, xn);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t i = 32 * k + lane;
+      const uint64_t q = c + i;
+      const uint32_t b0 = hp_byte(wc, xc, i), b1 = hp_byte(wc, xc, i + 1), b2 = hp_byte(wc, xc, i + 2);
+      const bool valid = q < e && q + MIN_MATCH <= n;
+      const uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, h);
+      const unsigned lower = peers & ((1u << lane) - 1);
+      uint32_t d = 0;
+      if (valid) {
+        if (lower) {
+          d = lane - (31 - __clz(lower));
+        } else {
+          const uint32_t r = head[h];
+          d = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
+        }
+      }
+      __syncwarp();
+      if (valid && (peers >> lane) == 1u) head[h] = (uint16_t)(q - s + 1);
+      __syncwarp();
+      if (q < e) out[q] = (uint16_t)d;
+    }
+    wc = wn;
+    xc = xn;
+  }
+  __syncwarp();
+  uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)blockIdx.x * 32768);
+  for (int i = lane; i < 32768 * 2 / 16; i += 32) dst[i] = h4[i];
+}
+
+__global__ void k_hash_fix(const LaneDev* __restrict__ lanes, int nlanes, const uint64_t* __restrict__ lp,
+                           const uint32_t* __restrict__ seg0, uint64_t total, uint16_t* __restrict__ pd,
+                           const uint16_t* __restrict__ seg_heads) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nlanes - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (lp[mid] <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    const LaneDev& L = lanes[lo];
+    const uint64_t q = g - lp[lo];
+    uint16_t* slot = pd + L.pbase + q;
+    if (*slot != 0xffff) continue;
+    const uint64_t seg = q / HP4_SEG;
+    uint32_t d = 0;
+    if (seg > 0) {
+      const uint32_t h =
+          (((uint32_t)__ldg(L.src + q) << 10) ^ ((uint32_t)__ldg(L.src + q + 1) << 5) ^ __ldg(L.src + q + 2)) & 0x7fff;
+      const uint32_t r = seg_heads[(uint64_t)(seg0[lo] + seg - 1) * 32768 + h];
+      if (r) {
+        const uint64_t pred = (seg - 1) * HP4_SEG + r - 1;
+        const uint64_t dd = q - pred;
+        d = dd < WSIZE ? (uint32_t)dd : 0;
+      }
+    }
+    *slot = (uint16_t)d;
+  }
+}
+
+static int hash_prev_two_phase(Workspace& sortws, Workspace& W, const LaneDev* d_lanes, int nl,
+                               const std::vector<uint64_t>& lane_prefix, uint16_t* d_pd, cudaStream_t st) {
+  std::vector<WorkItem> work;
+  std::vector<uint32_t> seg0(nl);
+  for (int i = 0; i < nl; i++) {
+    seg0[i] = (uint32_t)work.size();
+    const uint64_t n = lane_prefix[i + 1] - lane_prefix[i];
+    for (uint64_t s = 0; s < n; s += HP4_SEG) work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
+  }
+  if (work.empty()) return BB_OK;
+  int rc = sortws.reserve(2ull * 32768 * work.size() + 4096);
+  if (rc) return rc;
+  uint16_t* heads = sortws.take<uint16_t>(32768ull * work.size());
+  WorkItem* d_work = W.take<WorkItem>(work.size());
+  uint32_t* d_seg0 = W.take<uint32_t>(nl);
+  uint64_t* d_lp = W.take<uint64_t>(nl + 1);
+  BB_CUDA_TRY(cudaMemcpyAsync(d_work, work.data(), sizeof(WorkItem) * work.size(), cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_seg0, seg0.data(), 4 * nl, cudaMemcpyHostToDevice, st));
+  BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
+  k_hash_prev4<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
+  BB_LAUNCH_CHECK();
+  k_hash_fix<<<grid_for(lane_prefix[nl], 256, 16), 256, 0, st>>>(d_lanes, nl, d_lp, d_seg0, lane_prefix[nl], d_pd,
+                                                                  heads);
+  BB_LAUNCH_CHECK();
+  return BB_OK;
+}
+
 // K3 (device-wide sort): every position of every lane gets the key
 // (lane << 16 | hash) -- or (lane << 16 | 0x8000) when fewer than 3 bytes
 // remain -- and one stable LSD radix sort (CUB onesweep) brings equal hashes of
@@ -1636,6 +1754,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev4, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
     e->tables_ready = true;
   }
@@ -1710,7 +1829,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   need += al(sizeof(LaneSyms) * nl) + al(sizeof(BlockInfo) * blk_total) + al(sizeof(BlockCodes) * blk_total);
   need += al(HDR_BYTES * (size_t)blk_total) + al(sizeof(BlockPlan) * blk_total);
   need += al(8 * nl) + al(sizeof(uint8_t*) * nl) + al(8 * nc) + al(4 * nc) + al(sizeof(Adl) * ad_work.size() + 16);
-  need += 64 * 256 + al(8 * (nl + 1));
+  need += 64 * 256 + 2 * al(8 * (nl + 1)) + al(4 * nl) + al(sizeof(WorkItem) * (pos_total / HP4_SEG + nl + 1));
   int rc = e->ws.reserve(need);
   if (rc) return rc;
   Workspace& W = e->ws;
@@ -1770,9 +1889,9 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   if (npos_exact && k3_sorted) {
     rc = hash_prev_sorted(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st, &T);
     if (rc) return rc;
-  } else if (!hp_work.empty()) {
-    k_hash_prev3<<<(unsigned)hp_work.size(), 32, 65536, st>>>(d_lanes, d_hp, d_pd);
-    BB_LAUNCH_CHECK();
+  } else if (npos_exact) {
+    rc = hash_prev_two_phase(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
+    if (rc) return rc;
   }
   T.mark("deflate.profile");
   if (!pf_work.empty()) {
@@ -1903,10 +2022,15 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
     rc = hash_prev_sorted(sw, w2, dl, 1, lp, d_pd, st);
     if (rc) return rc;
     BB_CUDA_TRY(cudaStreamSynchronize(st));
-  } else if (!hp.empty()) {
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    k_hash_prev3<<<(unsigned)hp.size(), 32, 65536, st>>>(dl, dh, d_pd);
-    BB_LAUNCH_CHECK();
+  } else if (n) {
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev4, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    Workspace sw, w2;
+    int rc = w2.reserve(4096 + 16 * (n / HP4_SEG + 2));
+    if (rc) return rc;
+    std::vector<uint64_t> lp{0, n};
+    rc = hash_prev_two_phase(sw, w2, dl, 1, lp, d_pd, st);
+    if (rc) return rc;
+    BB_CUDA_TRY(cudaStreamSynchronize(st));
   }
   if (!pf.empty() && d_prof) {
     size_t smem = 4 * PF_WIN;
