@@ -356,28 +356,43 @@ __global__ void __launch_bounds__(32) k_hash_prev4(const LaneDev* __restrict__ l
   for (uint64_t c = s; c < e; c += 128) {
     uint32_t wn = 0, xn = 0;
     if (c + 128 < e) hp_load_tile(src, n, c + 128, lane, wn, xn);
+    // independent work of the 4 sub-steps first (hashes, same-hash groups) ...
+    uint32_t h[4];
+    unsigned peers[4];
+    bool valid[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       const uint32_t i = 32 * k + lane;
       const uint64_t q = c + i;
       const uint32_t b0 = hp_byte(wc, xc, i), b1 = hp_byte(wc, xc, i + 1), b2 = hp_byte(wc, xc, i + 2);
-      const bool valid = q < e && q + MIN_MATCH <= n;
-      const uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, h);
-      const unsigned lower = peers & ((1u << lane) - 1);
-      uint32_t d = 0;
-      if (valid) {
+      valid[k] = q < e && q + MIN_MATCH <= n;
+      h[k] = valid[k] ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) peers[k] = __match_any_sync(0xffffffffu, h[k]);
+    // ... then the in-order head table traffic
+    uint32_t d[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t q = c + 32 * k + lane;
+      const unsigned lower = peers[k] & ((1u << lane) - 1);
+      d[k] = 0;
+      if (valid[k]) {
         if (lower) {
-          d = lane - (31 - __clz(lower));
+          d[k] = lane - (31 - __clz(lower));
         } else {
-          const uint32_t r = head[h];
-          d = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
+          const uint32_t r = head[h[k]];
+          d[k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
         }
       }
       __syncwarp();
-      if (valid && (peers >> lane) == 1u) head[h] = (uint16_t)(q - s + 1);
+      if (valid[k] && (peers[k] >> lane) == 1u) head[h[k]] = (uint16_t)(q - s + 1);
       __syncwarp();
-      if (q < e) out[q] = (uint16_t)d;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t q = c + 32 * k + lane;
+      if (q < e) out[q] = (uint16_t)d[k];
     }
     wc = wn;
     xc = xn;
