@@ -186,8 +186,15 @@ __device__ __forceinline__ uint64_t slides_at(uint64_t t, uint64_t n) {
 // resolving same-hash lanes inside the warp.
 __device__ __forceinline__ void hp_load_tile(const uint8_t* src, uint64_t n, uint64_t c, int lane, uint32_t& w,
                                              uint32_t& x) {
-  // lane holds bytes [c + 4 lane, c + 4 lane + 4); x = bytes [c + 128, c + 132)
-  uint64_t a = c + 4 * (uint64_t)lane;
+  // lane holds bytes [c + 4 lane, c + 4 lane + 4); x = bytes [c + 128, c + 132).
+  // Word-aligned tiles away from the end are single 32-bit loads whose values
+  // are first used one tile later (so the prefetch really overlaps).
+  const uint64_t a = c + 4 * (uint64_t)lane;
+  if (((reinterpret_cast<uintptr_t>(src) + c) & 3) == 0 && c + 132 <= n) {
+    w = __ldg(reinterpret_cast<const uint32_t*>(src + a));
+    x = __ldg(reinterpret_cast<const uint32_t*>(src + c + 128));
+    return;
+  }
   w = 0;
 #pragma unroll
   for (int t = 0; t < 4; t++)
