@@ -935,7 +935,7 @@ struct TreesState {
   TreeArr<L_CODES> lt;
   TreeArr<D_CODES> dt;
   TreeArr<BL_CODES> blt;
-  uint64_t heap[HEAP_SIZE];
+  alignas(16) uint64_t heap[HEAP_SIZE + 1];
   uint16_t bl_count[16];
   uint64_t opt_len, static_len;
   int lmax, dmax, blmax;
@@ -954,9 +954,11 @@ __device__ __forceinline__ void t_down(uint64_t* heap, int heap_len, int k) {
   const uint64_t vk = v >> 16;
   int j = k << 1;
   while (j <= heap_len) {
-    uint64_t hj = heap[j];
+    // j is even: both sons in one 128-bit shared load (heap is 16-byte aligned)
+    const ulonglong2 sons = *reinterpret_cast<const ulonglong2*>(heap + j);
+    uint64_t hj = sons.x;
     if (j < heap_len) {
-      uint64_t hj1 = heap[j + 1];
+      const uint64_t hj1 = sons.y;
       if ((hj1 >> 16) <= (hj >> 16)) {
         j++;
         hj = hj1;
