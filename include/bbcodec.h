@@ -18,6 +18,9 @@
  *   bb_compress_batch               the stage hand-off's per-micro-batch compress calls
  *                                   src/wire.cpp:406-411,496-501 (batched into one pipeline)
  *   bb_decompress_batch             the per-micro-batch decompress calls src/wire.cpp:484-491,581-585
+ *   bb_pack_sd                      encode_packed(pack(per_request)) src/specdec.cpp:153-165,192-198,
+ *                                   include/beeplan/specdec.hpp (PackedBatch)
+ *   bb_unpack_sd                    decode_packed's checks src/specdec.cpp:167-180,200-220
  *
  * Status codes map 1:1 onto the reference exception types (include/beeplan/errors.hpp:40-56).
  * All device entry points are stream-ordered; those returning a size on the host
@@ -41,7 +44,9 @@ typedef enum {
   BB_CORRUPT_CONTAINER = 4, /* beeplan::CorruptContainer */
   BB_ERROR = 5,             /* beeplan::Error */
   BB_CUDA_ERROR = 6,        /* CUDA runtime failure (no reference equivalent) */
-  BB_INVALID_ARG = 7        /* caller error: null pointer / buffer too small */
+  BB_INVALID_ARG = 7,       /* caller error: null pointer / buffer too small */
+  BB_CORRUPT_OFFSETS = 8,   /* beeplan::CorruptOffsets */
+  BB_DIM_MISMATCH = 9       /* beeplan::DimMismatch */
 } bb_status;
 
 enum { BB_BACKEND_IDENTITY = 0, BB_BACKEND_DEFLATE = 1 };
@@ -107,6 +112,20 @@ BB_API int bb_split_host(bb_ctx* ctx, const uint8_t* h_stream, size_t n_bytes, u
 BB_API int bb_merge_host(bb_ctx* ctx, const uint8_t* h_high, const uint8_t* h_low, size_t count,
                   uint8_t* h_stream);
 BB_API int bb_histogram256_host(bb_ctx* ctx, const uint8_t* h_data, size_t n, uint64_t* h_counts);
+
+/* ---- speculative-decoding payloads (PackedSd frames) -------------------- */
+/* Wire image: u32 count (= n_requests + 1) | u32 offsets[count] | f32 payload, LE. */
+BB_API size_t bb_packed_bound(size_t n_rows, size_t hidden_dim, uint32_t n_requests);
+/* d_rows: [n_rows, hidden_dim] f32 token-tree states; d_keep[n_rows] != 0 keeps a row;
+ * h_request_rows[n_requests + 1]: request r owns rows [h_request_rows[r], h_request_rows[r+1]).
+ * Writes encode_packed(pack(kept rows per request)) to d_out; synchronizes the stream. */
+BB_API int bb_pack_sd(const float* d_rows, size_t n_rows, size_t hidden_dim, const uint8_t* d_keep,
+                      const uint32_t* h_request_rows, uint32_t n_requests, uint8_t* d_out, size_t out_cap,
+                      size_t* out_len, void* stream);
+/* Validates a packed image in HBM (decode_packed's CorruptOffsets rules) and returns its
+ * offsets (h_offsets may be NULL to query *n_offsets) and the payload's byte offset. */
+BB_API int bb_unpack_sd(const uint8_t* d_in, size_t n, size_t hidden_dim, uint32_t* h_offsets,
+                        size_t offsets_cap, uint32_t* n_offsets, size_t* payload_offset, void* stream);
 
 /* ---- instrumentation ---------------------------------------------------- */
 /* Number of kernels this library launched (process-wide, monotonic). */

@@ -161,6 +161,13 @@ class Reference:
         L.bbref_entropy.argtypes = [_u8p, C.c_size_t]
         L.bbref_last_error.restype = C.c_char_p
         L.bbref_free.argtypes = [C.c_void_p]
+        L.bbref_pack_encode.restype = C.c_int
+        L.bbref_pack_encode.argtypes = [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_uint),
+                                        C.c_uint, pp, C.POINTER(C.c_size_t)]
+        L.bbref_decode_packed.restype = C.c_int
+        L.bbref_decode_packed.argtypes = [_u8p, C.c_size_t, C.c_size_t, pp, C.POINTER(C.c_size_t)]
+        L.bbref_unpack_check.restype = C.c_int
+        L.bbref_unpack_check.argtypes = [C.POINTER(C.c_uint), C.c_size_t, C.c_size_t, C.c_size_t]
         self.lib = L
 
     def _take(self, rc, p, n):
@@ -201,3 +208,25 @@ class Reference:
 
     def entropy(self, data: bytes) -> float:
         return self.lib.bbref_entropy(_buf(data), len(data))
+
+    def pack_encode(self, per_request) -> bytes:
+        """encode_packed(pack(per_request)); per_request = list of lists of float sequences."""
+        import numpy as np
+        vecs = [np.asarray(v, dtype=np.float32).reshape(-1) for st in per_request for v in st]
+        flat = np.concatenate(vecs) if vecs else np.zeros(1, np.float32)
+        dims = (C.c_size_t * max(1, len(vecs)))(*[v.size for v in vecs])
+        counts = (C.c_uint * max(1, len(per_request)))(*[len(st) for st in per_request])
+        p, n = _u8p(), C.c_size_t()
+        rc = self.lib.bbref_pack_encode(flat.ctypes.data, dims, counts, len(per_request), C.byref(p),
+                                        C.byref(n))
+        return self._take(rc, p, n)
+
+    def decode_packed(self, data: bytes, hidden_dim: int) -> bytes:
+        """encode_packed(decode_packed(data, hidden_dim)) (raises OracleError 8 = CorruptOffsets)."""
+        p, n = _u8p(), C.c_size_t()
+        rc = self.lib.bbref_decode_packed(_buf(data), len(data), hidden_dim, C.byref(p), C.byref(n))
+        return self._take(rc, p, n)
+
+    def unpack_check(self, offsets, hidden_dim: int, payload_floats: int) -> int:
+        arr = (C.c_uint * max(1, len(offsets)))(*offsets)
+        return self.lib.bbref_unpack_check(arr, len(offsets), hidden_dim, payload_floats)

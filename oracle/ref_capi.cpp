@@ -10,6 +10,7 @@
 //   beeplan::parse_container + decompress     (reference codec.cpp:142-161,181-192)
 //   beeplan::synth_gaussian_fp16              (reference synth.cpp:66-94)
 //   beeplan::entropy_bits_per_byte            (reference codec.cpp:113-125)
+//   beeplan::pack / encode_packed / decode_packed / unpack (reference specdec.cpp:153-220)
 // Status codes follow include/bbcodec.h (bb_status).
 #include <cstdlib>
 #include <cstring>
@@ -18,6 +19,7 @@
 
 #include "beeplan/codec.hpp"
 #include "beeplan/errors.hpp"
+#include "beeplan/specdec.hpp"
 #include "beeplan/synth.hpp"
 
 namespace {
@@ -38,6 +40,12 @@ int map_exception() {
   } catch (const beeplan::CorruptContainer& e) {
     g_err = e.what();
     return 4;
+  } catch (const beeplan::CorruptOffsets& e) {
+    g_err = e.what();
+    return 8;
+  } catch (const beeplan::DimMismatch& e) {
+    g_err = e.what();
+    return 9;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 5;
@@ -126,6 +134,55 @@ int bbref_synth_fp16(size_t elements, unsigned long long seed, unsigned char* ou
 double bbref_entropy(const unsigned char* in, size_t n) {
   beeplan::Bytes b(in, in + n);
   return beeplan::entropy_bits_per_byte(b);
+}
+
+// encode_packed(pack(per_request)): request r holds req_counts[r] vectors, vector v has
+// row_dims[v] floats; the vectors are concatenated in `flat`.
+int bbref_pack_encode(const float* flat, const size_t* row_dims, const unsigned* req_counts,
+                      unsigned n_requests, unsigned char** out, size_t* out_len) {
+  try {
+    std::vector<beeplan::HiddenStates> per_request(n_requests);
+    size_t v = 0, f = 0;
+    for (unsigned r = 0; r < n_requests; ++r)
+      for (unsigned k = 0; k < req_counts[r]; ++k, ++v) {
+        per_request[r].emplace_back(flat + f, flat + f + row_dims[v]);
+        f += row_dims[v];
+      }
+    beeplan::Bytes wire = beeplan::encode_packed(beeplan::pack(per_request));
+    *out = dup_bytes(wire);
+    *out_len = wire.size();
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// encode_packed(decode_packed(data, hidden_dim)): status parity + round trip.
+int bbref_decode_packed(const unsigned char* in, size_t n, size_t hidden_dim, unsigned char** out,
+                        size_t* out_len) {
+  try {
+    beeplan::Bytes data(in, in + n);
+    beeplan::Bytes wire = beeplan::encode_packed(beeplan::decode_packed(data, hidden_dim));
+    *out = dup_bytes(wire);
+    *out_len = wire.size();
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// unpack(PackedBatch{hidden_dim, payload, offsets}) validity (CorruptOffsets).
+int bbref_unpack_check(const unsigned* offsets, size_t n_offsets, size_t hidden_dim, size_t payload_floats) {
+  try {
+    beeplan::PackedBatch b;
+    b.hidden_dim = hidden_dim;
+    b.offsets.assign(offsets, offsets + n_offsets);
+    b.payload.assign(payload_floats, 0.0f);
+    (void)beeplan::unpack(b);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
 }
 
 }  // extern "C"

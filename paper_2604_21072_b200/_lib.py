@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libbbcodec.so")
 
 BB_OK, BB_ODD_LENGTH, BB_LANE_MISMATCH, BB_BACKEND_UNKNOWN = 0, 1, 2, 3
 BB_CORRUPT_CONTAINER, BB_ERROR, BB_CUDA_ERROR, BB_INVALID_ARG = 4, 5, 6, 7
+BB_CORRUPT_OFFSETS, BB_DIM_MISMATCH = 8, 9
 
 EXPORTS = [
     "bb_last_error", "bb_version", "bb_ctx_create", "bb_ctx_destroy", "bb_split", "bb_merge",
@@ -21,7 +22,7 @@ EXPORTS = [
     "bb_decompress_batch", "bb_backend_bound", "bb_backend_encode", "bb_backend_decode",
     "bb_compress_host", "bb_decompress_host", "bb_backend_encode_host", "bb_backend_decode_host",
     "bb_split_host", "bb_merge_host", "bb_histogram256_host", "bb_kernel_launches",
-    "bb_stage_timing", "bb_stage_report",
+    "bb_stage_timing", "bb_stage_report", "bb_packed_bound", "bb_pack_sd", "bb_unpack_sd",
 ]
 
 _u8p = C.c_void_p
@@ -70,6 +71,12 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         L.bb_split_host.argtypes = [C.c_void_p, C.c_char_p, _sz, _u8p, _u8p]
         L.bb_merge_host.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, _sz, _u8p]
         L.bb_histogram256_host.argtypes = [C.c_void_p, C.c_char_p, _sz, _u8p]
+        L.bb_packed_bound.restype = _sz
+        L.bb_packed_bound.argtypes = [_sz, _sz, C.c_uint32]
+        L.bb_pack_sd.argtypes = [_u8p, _sz, _sz, _u8p, C.POINTER(C.c_uint32), C.c_uint32, _u8p, _sz,
+                                 _szp, C.c_void_p]
+        L.bb_unpack_sd.argtypes = [_u8p, _sz, _sz, C.POINTER(C.c_uint32), _sz, C.POINTER(C.c_uint32),
+                                   _szp, C.c_void_p]
         L.bb_kernel_launches.restype = C.c_uint64
         L.bb_stage_timing.argtypes = [C.c_int]
         L.bb_stage_report.restype = C.c_char_p

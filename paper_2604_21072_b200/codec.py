@@ -53,8 +53,16 @@ class CudaError(Error):
     pass
 
 
+class CorruptOffsets(Error):
+    """beeplan::CorruptOffsets (errors.hpp:71)"""
+
+
+class DimMismatch(Error):
+    """beeplan::DimMismatch (errors.hpp:67)"""
+
+
 _STATUS = {1: OddLength, 2: LaneLengthMismatch, 3: BackendUnknown, 4: CorruptContainer, 5: Error,
-           6: CudaError, 7: ValueError}
+           6: CudaError, 7: ValueError, 8: CorruptOffsets, 9: DimMismatch}
 
 
 def _check(rc: int) -> None:

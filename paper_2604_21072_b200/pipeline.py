@@ -195,10 +195,11 @@ class StageRing:
         return out
 
 
-def build_frames(containers, batch_id: int, flags: int, device):
-    """BBF1 frames on the device: host-built 20-byte headers + container bytes."""
+def build_frames(containers, batch_id: int, flags: int, device, msg_type: int = T_ACTIVATIONS):
+    """BBF1 frames on the device: host-built 20-byte headers + container bytes
+    (msg_type T_PACKED_SD for speculative-decoding token-tree payloads)."""
     import torch
-    hdrs = b"".join(frame_header(T_ACTIVATIONS, batch_id, m, flags, int(c.numel()))
+    hdrs = b"".join(frame_header(msg_type, batch_id, m, flags, int(c.numel()))
                     for m, c in enumerate(containers))
     h = torch.frombuffer(bytearray(hdrs), dtype=torch.uint8).to(device, non_blocking=True)
     return [torch.cat([h[FRAME_HEADER * m:FRAME_HEADER * (m + 1)], c]) for m, c in enumerate(containers)]

@@ -44,3 +44,40 @@ def make_input(spec: str, oracle=None) -> bytes:
             out += bytes([int(rng.integers(0, 4))]) * int(rng.integers(1, 601))
         return bytes(out[:n])
     raise ValueError(spec)
+
+
+def sd_tree(spec: str):
+    """Speculative-decoding token-tree batch (config 3 shape family), numpy only.
+
+    spec = sdtree:<requests>:<nodes>:<dim>:<seed>:<keep_percent>:<kind>
+      nodes per request is ragged: nodes - U[0, nodes/4] (some requests may be empty when
+      nodes is small); kind "f32" = N(0,1) floats, "bf16up" = bf16-representable values
+      (low 16 bits zero, as a bf16 model's states upcast), "special" = f32 with NaN/Inf/-0
+      payloads.
+    Returns (rows float32 [R, dim], keep uint8 [R], request_rows list[int], per_request lists).
+    """
+    _, nreq, nodes, dim, seed, keep_pct, kind = spec.split(":")
+    nreq, nodes, dim, seed, keep_pct = int(nreq), int(nodes), int(dim), int(seed), int(keep_pct)
+    rng = np.random.default_rng(seed)
+    counts = [max(0, nodes - int(rng.integers(0, nodes // 4 + 1))) for _ in range(nreq)]
+    total = sum(counts)
+    rows = rng.standard_normal((total, dim), dtype=np.float32)
+    if kind == "bf16up":
+        rows = (rows.view(np.uint32) & np.uint32(0xFFFF0000)).view(np.float32)
+    elif kind == "special":
+        bits = rows.view(np.uint32).copy()
+        sel = rng.integers(0, 64, bits.shape)
+        bits[sel == 0] = 0x7FC00001  # quiet NaN with payload
+        bits[sel == 1] = 0x7F800000  # +inf
+        bits[sel == 2] = 0x80000000  # -0
+        bits[sel == 3] = 0x00000001  # denormal
+        rows = bits.view(np.float32)
+    keep = (rng.integers(0, 100, total) < keep_pct).astype(np.uint8)
+    request_rows = [0]
+    for c in counts:
+        request_rows.append(request_rows[-1] + c)
+    per_request = []
+    for r in range(nreq):
+        lo, hi = request_rows[r], request_rows[r + 1]
+        per_request.append([rows[i] for i in range(lo, hi) if keep[i]])
+    return rows, keep, request_rows, per_request
