@@ -21,6 +21,8 @@
  *   bb_pack_sd                      encode_packed(pack(per_request)) src/specdec.cpp:153-165,192-198,
  *                                   include/beeplan/specdec.hpp (PackedBatch)
  *   bb_unpack_sd                    decode_packed's checks src/specdec.cpp:167-180,200-220
+ *   bb_gather_pages                 KV offload chunk producer (paged cache -> contiguous chunk);
+ *                                   the reference only models it: src/cost_model.cpp:30-47
  *
  * Status codes map 1:1 onto the reference exception types (include/beeplan/errors.hpp:40-56).
  * All device entry points are stream-ordered; those returning a size on the host
@@ -126,6 +128,12 @@ BB_API int bb_pack_sd(const float* d_rows, size_t n_rows, size_t hidden_dim, con
  * offsets (h_offsets may be NULL to query *n_offsets) and the payload's byte offset. */
 BB_API int bb_unpack_sd(const uint8_t* d_in, size_t n, size_t hidden_dim, uint32_t* h_offsets,
                         size_t offsets_cap, uint32_t* n_offsets, size_t* payload_offset, void* stream);
+
+/* ---- KV-cache offload chunks ------------------------------------------ */
+/* out[p] = pool[page_ids[p]] for p < n_pages (page_bytes each; page_ids in device memory).
+ * BB_INVALID_ARG when an id is >= n_pool_pages.  Synchronizes the stream. */
+BB_API int bb_gather_pages(const uint8_t* d_pool, size_t n_pool_pages, size_t page_bytes,
+                           const uint32_t* d_page_ids, uint32_t n_pages, uint8_t* d_out, void* stream);
 
 /* ---- instrumentation ---------------------------------------------------- */
 /* Number of kernels this library launched (process-wide, monotonic). */

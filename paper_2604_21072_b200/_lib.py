@@ -23,6 +23,7 @@ EXPORTS = [
     "bb_compress_host", "bb_decompress_host", "bb_backend_encode_host", "bb_backend_decode_host",
     "bb_split_host", "bb_merge_host", "bb_histogram256_host", "bb_kernel_launches",
     "bb_stage_timing", "bb_stage_report", "bb_packed_bound", "bb_pack_sd", "bb_unpack_sd",
+    "bb_gather_pages",
 ]
 
 _u8p = C.c_void_p
@@ -77,6 +78,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
                                  _szp, C.c_void_p]
         L.bb_unpack_sd.argtypes = [_u8p, _sz, _sz, C.POINTER(C.c_uint32), _sz, C.POINTER(C.c_uint32),
                                    _szp, C.c_void_p]
+        L.bb_gather_pages.argtypes = [_u8p, _sz, _sz, _u8p, C.c_uint32, _u8p, C.c_void_p]
         L.bb_kernel_launches.restype = C.c_uint64
         L.bb_stage_timing.argtypes = [C.c_int]
         L.bb_stage_report.restype = C.c_char_p
