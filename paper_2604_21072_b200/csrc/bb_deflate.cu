@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "bb_common.cuh"
@@ -409,6 +410,208 @@ __global__ void __launch_bounds__(32) k_hash_prev4(const LaneDev* __restrict__ l
   for (int i = lane; i < 32768 * 2 / 16; i += 32) dst[i] = h4[i];
 }
 
+// K3 (block-parallel, current): one 1024-thread CTA per SM walks 32 Ki-position
+// segments 1024 positions (one chunk) at a time.  Within a warp,
+// __match_any_sync finds the previous lane with the same hash.  Across the 32
+// warps of a chunk, every same-hash group's leader (its last lane) sets its
+// warp's bit in a per-hash mask M[h] and enters (h, lane) in its warp's small
+// open-addressed table T.  A position without an earlier same-hash lane in its
+// warp takes the highest earlier warp in M[h] and looks its lane up in that
+// warp's T, or else reads the segment's head table H (last position of h in
+// earlier chunks).  The chunk's last group of each hash then updates H and
+// clears M[h]; leaders empty their T slots.  Three barriers per 1024 positions
+// instead of one in-order table update per 32; positions whose hash is new to the
+// segment get 0xffff and are resolved by k_hash_fix from the previous segment's
+// final table, as before.
+constexpr int HP5_THREADS = 1024;
+constexpr int HP5_TSLOTS = 64;  // per-warp (hash, lane) table
+constexpr size_t HP5_SMEM = 32768 * 4 + 32768 * 2 + (HP5_THREADS / 32) * HP5_TSLOTS * 4;
+
+__global__ void __launch_bounds__(HP5_THREADS, 1) k_hash_prev5(const LaneDev* __restrict__ lanes,
+                                                               const WorkItem* __restrict__ work, uint32_t nwork,
+                                                               uint16_t* __restrict__ pd,
+                                                               uint16_t* __restrict__ seg_heads) {
+  extern __shared__ __align__(16) uint8_t hp5_smem[];
+  uint32_t* M = reinterpret_cast<uint32_t*>(hp5_smem);              // 32768 warp masks
+  uint16_t* H = reinterpret_cast<uint16_t*>(hp5_smem + 32768 * 4);  // position - s + 1 (0 = none)
+  uint32_t* T = reinterpret_cast<uint32_t*>(hp5_smem + 32768 * 6);  // [warp][slot] = h << 8 | lane
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned below = (1u << lane) - 1;
+  {
+    uint4* m4 = reinterpret_cast<uint4*>(M);
+    for (int i = tid; i < 32768 * 4 / 16; i += HP5_THREADS) m4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < (HP5_THREADS / 32) * HP5_TSLOTS; i += HP5_THREADS) T[i] = 0xffffffffu;
+  }
+  uint32_t* Tw = T + warp * HP5_TSLOTS;
+  for (uint32_t wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+    const WorkItem w = work[wi];
+    const LaneDev L = lanes[w.lane];
+    const uint64_t n = L.n;
+    const uint64_t s = w.start;
+    const uint64_t e = umin64(s + HP4_SEG, n);
+    const uint8_t* src = L.src;
+    uint16_t* out = pd + L.pbase;
+    {
+      uint4* h4 = reinterpret_cast<uint4*>(H);
+      for (int i = tid; i < 32768 * 2 / 16; i += HP5_THREADS) h4[i] = make_uint4(0, 0, 0, 0);
+    }
+    // bytes of the first chunk (prefetched one chunk ahead from then on)
+    uint32_t b0 = 0, b1 = 0, b2 = 0;
+    {
+      const uint64_t q = s + tid;
+      if (q + MIN_MATCH <= n) b0 = __ldg(src + q), b1 = __ldg(src + q + 1), b2 = __ldg(src + q + 2);
+    }
+    __syncthreads();
+    for (uint64_t c = s; c < e; c += HP5_THREADS) {
+      const uint64_t q = c + tid;
+      const bool valid = q < e && q + MIN_MATCH <= n;
+      const uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + tid;
+      {
+        const uint64_t qn = q + HP5_THREADS;
+        b0 = b1 = b2 = 0;
+        if (qn < e && qn + MIN_MATCH <= n) b0 = __ldg(src + qn), b1 = __ldg(src + qn + 1), b2 = __ldg(src + qn + 2);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, h);
+      const bool leader = valid && (peers >> lane) == 1u;  // last lane of its group in this warp
+      uint32_t slot = 0;
+      if (leader) {
+        atomicOr(&M[h], 1u << warp);
+        slot = h & (HP5_TSLOTS - 1);
+        while (atomicCAS(&Tw[slot], 0xffffffffu, (h << 8) | lane) != 0xffffffffu) slot = (slot + 1) & (HP5_TSLOTS - 1);
+      }
+      __syncthreads();
+      uint32_t d = 0;
+      bool last = false;
+      if (valid) {
+        const unsigned lower = peers & below;
+        const uint32_t m = M[h];
+        last = leader && (m >> warp) == 1u;
+        if (lower) {
+          d = lane - (31 - __clz(lower));
+        } else {
+          const uint32_t mb = m & ((1u << warp) - 1);
+          if (mb) {
+            const int w2 = 31 - __clz(mb);
+            const uint32_t* T2 = T + w2 * HP5_TSLOTS;
+            uint32_t sl = h & (HP5_TSLOTS - 1), v;
+            while (((v = T2[sl]) >> 8) != h) sl = (sl + 1) & (HP5_TSLOTS - 1);
+            d = (uint32_t)(tid - (w2 * 32 + (int)(v & 31)));
+          } else {
+            const uint32_t r = H[h];
+            d = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;
+          }
+        }
+      }
+      __syncthreads();
+      if (leader) Tw[slot] = 0xffffffffu;
+      if (last) {
+        H[h] = (uint16_t)(q - s + 1);
+        M[h] = 0;
+      }
+      if (q < e) out[q] = (uint16_t)d;
+      __syncthreads();
+    }
+    uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)wi * 32768);
+    const uint4* h4 = reinterpret_cast<const uint4*>(H);
+    for (int i = tid; i < 32768 * 2 / 16; i += HP5_THREADS) dst[i] = h4[i];
+    __syncthreads();
+  }
+}
+
+// K3 (warp per segment, deep prefetch): k_hash_prev4's in-order scan with the
+// segment's bytes prefetched HP6_D tiles (HP6_D x 128 positions) ahead into
+// registers, so the warp's serial head-table chain is not also waiting on DRAM,
+// and the three hash bytes of a position taken from two shuffled words.
+constexpr int HP6_D = 8;
+
+__device__ __forceinline__ uint32_t hp_hash_at(uint32_t w, uint32_t x, int k, int lane) {
+  // hash bytes of tile position i = 32 k + lane: words j = i / 4 and j + 1 (x past the tile)
+  const int j = 8 * k + (lane >> 2);
+  const uint32_t a = __shfl_sync(0xffffffffu, w, j & 31);
+  uint32_t b = __shfl_sync(0xffffffffu, w, (j + 1) & 31);
+  if (j == 31) b = x;
+  const uint32_t v = __funnelshift_r(a, b, 8 * (lane & 3));
+  return (((v & 0xff) << 10) ^ (((v >> 8) & 0xff) << 5) ^ ((v >> 16) & 0xff)) & 0x7fff;
+}
+
+__global__ void __launch_bounds__(32) k_hash_prev6(const LaneDev* __restrict__ lanes,
+                                                   const WorkItem* __restrict__ work, uint16_t* __restrict__ pd,
+                                                   uint16_t* __restrict__ seg_heads) {
+  extern __shared__ uint16_t hp6_head[];  // position - s + 1 (0 = none)
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + HP4_SEG, n);
+  const int lane = threadIdx.x;
+  uint16_t* head = hp6_head;
+  uint4* h4 = reinterpret_cast<uint4*>(head);
+  const uint8_t* src = L.src;
+  uint16_t* out = pd + L.pbase;
+  uint32_t cw[HP6_D], cx[HP6_D], nw[HP6_D], nx[HP6_D];
+#pragma unroll
+  for (int t = 0; t < HP6_D; t++) {
+    const uint64_t c = s + 128ull * t;
+    cw[t] = cx[t] = 0;
+    if (c < e) hp_load_tile(src, n, c, lane, cw[t], cx[t]);
+  }
+  for (int i = lane; i < 32768 * 2 / 16; i += 32) h4[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  for (uint64_t cs = s; cs < e; cs += 128ull * HP6_D) {
+#pragma unroll
+    for (int t = 0; t < HP6_D; t++) {
+      const uint64_t c = cs + 128ull * (HP6_D + t);
+      nw[t] = nx[t] = 0;
+      if (c < e) hp_load_tile(src, n, c, lane, nw[t], nx[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < HP6_D; t++) {
+      const uint64_t c = cs + 128ull * t;
+      if (c >= e) break;
+      uint32_t h[4];
+      unsigned peers[4];
+      bool valid[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint64_t q = c + 32 * k + lane;
+        valid[k] = q < e && q + MIN_MATCH <= n;
+        const uint32_t hh = hp_hash_at(cw[t], cx[t], k, lane);
+        h[k] = valid[k] ? hh : 0x10000u + lane;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) peers[k] = __match_any_sync(0xffffffffu, h[k]);
+      uint32_t d[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint64_t q = c + 32 * k + lane;
+        const unsigned lower = peers[k] & ((1u << lane) - 1);
+        d[k] = 0;
+        if (valid[k]) {
+          if (lower) {
+            d[k] = lane - (31 - __clz(lower));
+          } else {
+            const uint32_t r = head[h[k]];
+            d[k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
+          }
+        }
+        __syncwarp();
+        if (valid[k] && (peers[k] >> lane) == 1u) head[h[k]] = (uint16_t)(q - s + 1);
+        __syncwarp();
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint64_t q = c + 32 * k + lane;
+        if (q < e) out[q] = (uint16_t)d[k];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < HP6_D; t++) cw[t] = nw[t], cx[t] = nx[t];
+  }
+  __syncwarp();
+  uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)blockIdx.x * 32768);
+  for (int i = lane; i < 32768 * 2 / 16; i += 32) dst[i] = h4[i];
+}
+
 __global__ void k_hash_fix(const LaneDev* __restrict__ lanes, int nlanes, const uint64_t* __restrict__ lp,
                            const uint32_t* __restrict__ seg0, uint64_t total, uint16_t* __restrict__ pd,
                            const uint16_t* __restrict__ seg_heads) {
@@ -458,7 +661,15 @@ static int hash_prev_two_phase(Workspace& sortws, Workspace& W, const LaneDev* d
   BB_CUDA_TRY(cudaMemcpyAsync(d_work, work.data(), sizeof(WorkItem) * work.size(), cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_seg0, seg0.data(), 4 * nl, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
-  k_hash_prev4<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
+  static const int k3_variant = getenv("BB_K3_VARIANT") ? atoi(getenv("BB_K3_VARIANT")) : 6;
+  if (k3_variant == 4) {
+    k_hash_prev4<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
+  } else if (k3_variant == 6) {
+    k_hash_prev6<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
+  } else {
+    const unsigned grid = (unsigned)std::min<size_t>(work.size(), kNumSMs);
+    k_hash_prev5<<<grid, HP5_THREADS, HP5_SMEM, st>>>(d_lanes, d_work, (uint32_t)work.size(), d_pd, heads);
+  }
   BB_LAUNCH_CHECK();
   k_hash_fix<<<grid_for(lane_prefix[nl], 256, 16), 256, 0, st>>>(d_lanes, nl, d_lp, d_seg0, lane_prefix[nl], d_pd,
                                                                   heads);
@@ -682,6 +893,264 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile(const LaneDev* __rest
       res.y = r32 | flag;
     }
     prof[L.pbase + p] = res;
+  }
+}
+
+// K4 (current): the same first-maximum search with two changes that remove most
+// of the warp divergence of the chain walk:
+//  * window word = (1-based window index of the previous same-hash position,
+//    0 = none) | bytes (q, q+1) << 16, so a chain step is: load the candidate's
+//    word, load bytes (best-1, best) of the candidate, one byte_perm compare,
+//    and the next link is the low half -- the limit test "index > lim1" also
+//    catches "none";
+//  * a candidate passing the quick reject is not extended at once (which ran
+//    the extension loop for one lane while 31 waited).  It is parked in the
+//    lane's pending slot and extended later, together with the pending
+//    candidates of the other lanes: when some lane passes again while it still
+//    has one parked, at the budget-32 snapshot and at the end.  best only
+//    changes in those flushes, so a parked candidate is judged against exactly
+//    the best it was tested with, and a candidate tested while another was
+//    parked that fails the quick reject cannot beat the flushed best either (it
+//    mismatches at or before the old best).  Exact first-maximum semantics.
+__global__ void __launch_bounds__(PF_THREADS, 1) k_profile2(const LaneDev* __restrict__ lanes,
+                                                            const WorkItem* __restrict__ work,
+                                                            const uint16_t* __restrict__ pd,
+                                                            uint2* __restrict__ prof) {
+  extern __shared__ __align__(16) uint32_t w32[];
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + PF_SEG, n);
+  const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
+  const uint32_t wlen = (uint32_t)(e - wlo) + MAX_MATCH + 16;  // <= PF_WIN
+  const uint8_t* src = L.src;
+  const uint16_t* pdl = pd + L.pbase;
+  for (uint32_t i = threadIdx.x; i < wlen; i += blockDim.x) {
+    const uint64_t q = wlo + i;
+    uint32_t v = 0;
+    if (q < e) {
+      const uint32_t l = pdl[q];
+      if (l && l <= i) v = i - l + 1;  // predecessor inside the window
+    }
+    if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
+    if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
+    w32[i] = v;
+  }
+  __syncthreads();
+  const char* wb = reinterpret_cast<const char*>(w32);
+
+  for (uint64_t p0 = s; p0 < e; p0 += blockDim.x) {
+    const uint64_t p = p0 + threadIdx.x;
+    uint2 res = make_uint2(0, 0);
+    const uint32_t ip = (uint32_t)(p - wlo);
+    const uint32_t wp = p < e ? w32[ip] : 0;
+    const uint32_t c0 = wp & 0xffff;  // 1-based index of the first candidate
+    const uint32_t d0 = ip + 1 - c0;
+    bool alive = p < e && p + MIN_MATCH <= n && c0 != 0 && d0 <= MAX_DIST && wlo + c0 - 1 != 0;
+    // the warp walks while any lane is alive (uniform control flow)
+    uint32_t best = MIN_MATCH - 1, bestd = 0, r32 = 0, flag = 0;
+    uint32_t la = 0, nice = 0, maxl = 0, lim1 = 0, key = 0, off = 0, ic1 = 1, q0 = 0;
+    bool has = false;
+    if (alive) {
+      la = (uint32_t)umin64(n - p, 1u << 20);
+      nice = min(NICE_LENGTH, la);
+      maxl = min(MAX_MATCH, la);
+      const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
+      lim1 = limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0;
+      flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
+      key = (wp >> 16) | (w32[ip + best - 1] & 0xffff0000u);
+      off = 4 * (best - 1) + 2;  // byte offset from word (ic1 - 1) to the high half of word (ic1 + best - 2)
+      ic1 = c0;
+    }
+    // extend the parked candidate (lanes with one), judge it against best
+    auto flush = [&]() {
+      if (has) {
+        const uint32_t ic = q0 - 1;
+        uint32_t len = 2;
+        while (len < maxl) {
+          const uint32_t x = (w32[ic + len] ^ w32[ip + len]) >> 16;
+          if (x) {
+            len += (x & 0xff) == 0;
+            break;
+          }
+          len += 2;
+        }
+        len = min(len, maxl);
+        if (len > best) {
+          best = len;
+          bestd = ip - ic;
+          if (len >= nice) alive = false;
+          key = (wp >> 16) | (w32[ip + best - 1] & 0xffff0000u);
+          off = 4 * (best - 1) + 2;
+        }
+        has = false;
+      }
+    };
+    auto step = [&]() {
+      const uint32_t wc = *reinterpret_cast<const uint32_t*>(wb + 4 * (ic1 - 1));
+      uint32_t we = *reinterpret_cast<const uint16_t*>(wb + 4 * (ic1 - 1) + off);
+      bool pass = alive && __byte_perm(wc, we, 0x5432) == key;
+      if (__any_sync(0xffffffffu, pass && has)) {
+        flush();
+        we = *reinterpret_cast<const uint16_t*>(wb + 4 * (ic1 - 1) + off);
+        pass = alive && __byte_perm(wc, we, 0x5432) == key;
+      }
+      if (pass) {
+        q0 = ic1;
+        has = true;
+      }
+      const uint32_t nx = wc & 0xffff;
+      alive = alive && nx > lim1;
+      if (alive) ic1 = nx;
+    };
+    for (int cnt = 0; cnt < 32; cnt += 4) {
+      if (!__any_sync(0xffffffffu, alive)) break;
+      step(); step(); step(); step();
+    }
+    flush();
+    r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
+    for (int cnt = 32; cnt < (int)MAX_CHAIN; cnt += 4) {
+      if (!__any_sync(0xffffffffu, alive)) break;
+      step(); step(); step(); step();
+    }
+    flush();
+    res.x = prof_pack(best, bestd) | flag;
+    res.y = r32 | flag;
+    if (p < e) prof[L.pbase + p] = res;
+  }
+}
+
+// K4 (current): first-maximum chain search with the passes of each lane
+// batched.  Window word (shared memory, word 0 = a dead-end sentinel):
+// (1-based window index of the previous same-hash position, 0 = none) | bytes
+// (q, q+1) << 16.  A chain step is: the candidate's word, the candidate's bytes
+// (best-1, best), one byte_perm compare against the lane's key, and the next
+// link; a lane whose chain ends moves to the sentinel with a key that cannot
+// match, so all 32 lanes step in lock-step without per-lane control flow.
+// Candidates that pass the quick reject are only recorded (a bit per step of
+// the batch); after every batch the lanes extend their recorded candidates in
+// chain order, re-testing each against the best found so far.  best therefore
+// lags by at most one batch during the walk: a candidate that fails the quick
+// reject against the lagging best mismatches at or before it and cannot beat
+// the final best either, so the result is exactly zlib's first maximum.
+template <int B>
+__device__ __forceinline__ uint32_t pf_pick(const uint32_t (&c)[B], int t) {
+  uint32_t v = c[0];
+#pragma unroll
+  for (int k = 1; k < B; k++) v = t == k ? c[k] : v;
+  return v;
+}
+
+constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;  // sentinel word is 0: its byte_perm low half never equals 0xffff
+
+__global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __restrict__ lanes,
+                                                            const WorkItem* __restrict__ work,
+                                                            const uint16_t* __restrict__ pd,
+                                                            uint2* __restrict__ prof) {
+  extern __shared__ __align__(16) uint32_t w32[];
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + PF_SEG, n);
+  const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
+  const uint32_t wlen = (uint32_t)(e - wlo) + MAX_MATCH + 16;  // <= PF_WIN
+  const uint8_t* src = L.src;
+  const uint16_t* pdl = pd + L.pbase;
+  if (threadIdx.x == 0) w32[0] = 0;
+  for (uint32_t i = threadIdx.x; i < wlen; i += blockDim.x) {
+    const uint64_t q = wlo + i;
+    uint32_t v = 0;
+    if (q < e) {
+      const uint32_t l = pdl[q];
+      if (l && l <= i) v = i - l + 1;  // 1-based index of the predecessor inside the window
+    }
+    if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
+    if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
+    w32[i + 1] = v;
+  }
+  __syncthreads();
+  const char* wb = reinterpret_cast<const char*>(w32);
+
+  for (uint64_t p0 = s; p0 < e; p0 += blockDim.x) {
+    const uint64_t p = p0 + threadIdx.x;
+    const uint32_t ip1 = (uint32_t)(p - wlo) + 1;
+    const uint32_t wp = p < e ? w32[ip1] : 0;
+    const uint32_t c0 = wp & 0xffff;
+    const uint32_t d0 = ip1 - c0;
+    const bool live = p < e && p + MIN_MATCH <= n && c0 != 0 && d0 <= MAX_DIST && wlo + c0 - 1 != 0;
+    uint32_t best = MIN_MATCH - 1, bestd = 0, flag = 0, nice = 0, maxl = 0, lim1 = 0;
+    uint32_t ic1 = 0, key = PF_DEAD_KEY, off = 4 * (MIN_MATCH - 2) + 2;
+    if (live) {
+      const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
+      nice = min(NICE_LENGTH, la);
+      maxl = min(MAX_MATCH, la);
+      const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
+      lim1 = limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0;
+      flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
+      ic1 = c0;
+      key = (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u);
+    }
+    // one batch of B chain steps, then the recorded candidates in chain order
+    auto batch = [&](auto bsize) {
+      constexpr int B = decltype(bsize)::value;
+      uint32_t cand[B];
+      uint32_t mask = 0;
+#pragma unroll
+      for (int t = 0; t < B; t++) {
+        const uint32_t wc = *reinterpret_cast<const uint32_t*>(wb + 4 * ic1);
+        const uint32_t we = *reinterpret_cast<const uint16_t*>(wb + 4 * ic1 + off);
+        cand[t] = ic1;
+        mask |= __byte_perm(wc, we, 0x5432) == key ? 1u << t : 0u;
+        const uint32_t nx = wc & 0xffff;
+        const bool end = nx <= lim1;
+        ic1 = end ? 0 : nx;
+        key = end ? PF_DEAD_KEY : key;
+      }
+      if (__any_sync(0xffffffffu, mask != 0)) {
+        bool improved = false;
+        while (mask) {
+          const int t = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const uint32_t c = pf_pick(cand, t);
+          if ((((w32[c] ^ wp) | (w32[c + best - 1] ^ w32[ip1 + best - 1])) & 0xffff0000u) != 0) continue;
+          uint32_t len = 2;
+          while (len < maxl) {
+            const uint32_t x = (w32[c + len] ^ w32[ip1 + len]) >> 16;
+            if (x) {
+              len += (x & 0xff) == 0;
+              break;
+            }
+            len += 2;
+          }
+          len = min(len, maxl);
+          if (len > best) {
+            best = len;
+            bestd = ip1 - c;
+            improved = true;
+            if (len >= nice) {
+              mask = 0;
+              ic1 = 0;
+            }
+          }
+        }
+        if (improved) {
+          off = 4 * (best - 1) + 2;
+          key = ic1 ? (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u) : PF_DEAD_KEY;
+        }
+      }
+    };
+    for (int cnt = 0; cnt < 32; cnt += 4) {
+      if (!__any_sync(0xffffffffu, ic1 != 0)) break;
+      batch(std::integral_constant<int, 4>());
+    }
+    const uint32_t r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
+    for (int cnt = 32; cnt < (int)MAX_CHAIN; cnt += 8) {
+      if (!__any_sync(0xffffffffu, ic1 != 0)) break;
+      batch(std::integral_constant<int, 8>());
+    }
+    if (p < e) prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, live ? r32 | flag : 0);
   }
 }
 
@@ -1779,7 +2248,11 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev4, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HP5_SMEM));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile2, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
     e->tables_ready = true;
   }
   const int nl = (int)jobs.size();
@@ -1920,7 +2393,14 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   T.mark("deflate.profile");
   if (!pf_work.empty()) {
     size_t smem = 4 * PF_WIN;
-    k_profile<<<(unsigned)pf_work.size(), PF_THREADS, smem, st>>>(d_lanes, d_pf, d_pd, d_prof);
+    static const int k4_old = getenv("BB_K4_OLD") ? 1 : 0;
+    static const int k4_var = getenv("BB_K4_VARIANT") ? atoi(getenv("BB_K4_VARIANT")) : 3;
+    if (k4_old || k4_var == 1)
+      k_profile<<<(unsigned)pf_work.size(), PF_THREADS, smem, st>>>(d_lanes, d_pf, d_pd, d_prof);
+    else if (k4_var == 2)
+      k_profile2<<<(unsigned)pf_work.size(), PF_THREADS, smem, st>>>(d_lanes, d_pf, d_pd, d_prof);
+    else
+      k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, smem + 16, st>>>(d_lanes, d_pf, d_pd, d_prof);
     BB_LAUNCH_CHECK();
   }
   // K5: speculative parse, then fix-up rounds until no exit state changes
@@ -2024,6 +2504,8 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile2, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
   LaneDev d{};
   d.src = d_in;
   d.n = n;
@@ -2048,6 +2530,8 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
     BB_CUDA_TRY(cudaStreamSynchronize(st));
   } else if (n) {
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev4, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HP5_SMEM));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     Workspace sw, w2;
     int rc = w2.reserve(4096 + 16 * (n / HP4_SEG + 2));
     if (rc) return rc;
@@ -2058,7 +2542,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   }
   if (!pf.empty() && d_prof) {
     size_t smem = 4 * PF_WIN;
-    k_profile<<<(unsigned)pf.size(), PF_THREADS, smem, st>>>(dl, dp, d_pd, reinterpret_cast<uint2*>(d_prof));
+    k_profile3<<<(unsigned)pf.size(), PF_THREADS, smem + 16, st>>>(dl, dp, d_pd, reinterpret_cast<uint2*>(d_prof));
     BB_LAUNCH_CHECK();
   }
   BB_CUDA_TRY(cudaStreamSynchronize(st));

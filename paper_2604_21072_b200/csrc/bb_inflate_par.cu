@@ -473,6 +473,80 @@ __global__ void k_candidates(const PJob* __restrict__ jobs, const uint64_t* __re
 }
 
 
+// P1 (current): four stream bytes / 32 bit offsets per thread.  The cheap
+// header conditions (BTYPE = 10, HLIT <= 29, HDIST <= 29) are evaluated for all
+// 32 offsets at once on a 64-bit window (bit-sliced), and only the ~20 % that
+// survive run the code-length-code Kraft sum, which stops as soon as it is
+// over-subscribed.
+__global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __restrict__ blk_prefix, int njobs,
+                              uint32_t* __restrict__ sbm, int find_dynamic, uint64_t* __restrict__ surv,
+                              unsigned long long* __restrict__ surv_cnt, uint64_t surv_cap) {
+  const uint32_t j = (uint32_t)find_job(blk_prefix, njobs, blockIdx.x);
+  const PJob J = jobs[j];
+  const uint64_t T = (blockIdx.x - blk_prefix[j]) * 256ull + threadIdx.x;  // bytes [4T, 4T + 4)
+  const uint64_t B0 = 4 * T;
+  const int lane = threadIdx.x & 31;
+  uint32_t dbits = 0, sbits = 0;
+  if (B0 < J.n) {
+    const uint64_t nbits = 8 * J.n;
+    if (find_dynamic) {
+      const uint64_t x0 = peek64(J.src, J.n, 8 * B0), x1 = peek64(J.src, J.n, 8 * B0 + 64);
+      uint64_t m = ~(x0 >> 1) & (x0 >> 2);
+      m &= ~((x0 >> 4) & (x0 >> 5) & (x0 >> 6) & (x0 >> 7));
+      m &= ~((x0 >> 9) & (x0 >> 10) & (x0 >> 11) & (x0 >> 12));
+      uint32_t cm = (uint32_t)m;
+      // stream limits: b >= 16 and b + 17 <= 8 n
+      const uint64_t b0 = 8 * B0;
+      if (b0 < 16) cm &= 0xffffffffu << (uint32_t)(16 - b0);
+      if (b0 + 31 + 17 > nbits) {
+        const int64_t keep = (int64_t)nbits - 17 - (int64_t)b0 + 1;  // offsets i < keep are allowed
+        cm &= keep <= 0 ? 0u : (keep >= 32 ? 0xffffffffu : ((1u << keep) - 1));
+      }
+      while (cm) {
+        const uint32_t i = __ffs(cm) - 1;
+        cm &= cm - 1;
+        const uint32_t ncode = bits_at(x0, x1, i + 13, 4) + 4;
+        uint32_t kraft = 0;
+        for (uint32_t k = 0; k < ncode && kraft <= 128; k++) {
+          const uint32_t l = bits_at(x0, x1, i + 17 + 3 * k, 3);
+          kraft += l ? (128u >> l) : 0u;
+        }
+        if (kraft == 128) dbits |= 1u << i;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t B = B0 + k;
+      if (B >= 2 && B + 4 <= J.n) {
+        const uint32_t len = __ldg(J.src + B) | ((uint32_t)__ldg(J.src + B + 1) << 8);
+        const uint32_t nlen = __ldg(J.src + B + 2) | ((uint32_t)__ldg(J.src + B + 3) << 8);
+        if (len == (~nlen & 0xffff) && B + 4 + len <= J.n) sbits |= 1u << k;
+      }
+    }
+  }
+  {
+    const uint32_t cnt = __popc(dbits);
+    uint32_t pre = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+    unsigned long long base = 0;
+    if (lane == 0 && tot) base = atomicAdd(surv_cnt, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    uint64_t slot = base + pre - cnt;
+    for (uint32_t v = dbits; v; v &= v - 1, slot++)
+      if (slot < surv_cap) surv[slot] = ((uint64_t)j << 48) | (8 * B0 + (__ffs(v) - 1));
+  }
+  // stored bitmap: 8 lanes (32 bytes) per word
+  uint32_t wv = sbits << (4 * (lane & 7));
+  wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+  wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
+  wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
+  if ((lane & 7) == 0 && B0 < J.n + 32) sbm[J.sbm + (B0 >> 5)] = wv;
+}
+
 __global__ void k_verify_dynamic(const PJob* __restrict__ jobs, const uint64_t* __restrict__ surv,
                                  const unsigned long long* __restrict__ surv_cnt, uint64_t surv_cap,
                                  uint32_t* __restrict__ dbm, uint32_t* __restrict__ fail, int njobs) {
@@ -1563,7 +1637,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     p.nsub = (uint32_t)((p.expected + SUB - 1) / SUB);
     subs += p.nsub;
     for (uint32_t s = 0; s < p.nsub; s++) sub_job.push_back(i);
-    blk_prefix[i + 1] = blk_prefix[i] + (p.n + 255) / 256;
+    blk_prefix[i + 1] = blk_prefix[i] + (p.n + 1023) / 1024;
     chunk_base[i] = (uint32_t)chunk_job.size();
     for (uint64_t c = 0; c * PA_CHUNK < p.expected; c++) chunk_job.push_back(i);
   }
@@ -1617,8 +1691,8 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   // P1
   BB_CUDA_TRY(cudaMemsetAsync(d_surv_cnt, 0, 8, st));
   T.mark(find_dynamic ? "inflate.candidates_dyn" : "inflate.candidates_stored");
-  k_candidates<<<(unsigned)cand_blocks, 256, 0, st>>>(d_jobs, d_blk_prefix, nj, d_dbm, d_sbm,
-                                                          find_dynamic, d_surv, d_surv_cnt, surv_cap);
+  k_candidates4<<<(unsigned)cand_blocks, 256, 0, st>>>(d_jobs, d_blk_prefix, nj, d_sbm, find_dynamic, d_surv,
+                                                       d_surv_cnt, surv_cap);
   BB_LAUNCH_CHECK();
   if (find_dynamic) {
     T.mark("inflate.verify_headers");
