@@ -642,6 +642,59 @@ __global__ void k_hash_fix(const LaneDev* __restrict__ lanes, int nlanes, const 
   }
 }
 
+// k_hash_fix2: one CTA per segment, eight positions per thread and step
+// (one 16-byte load of their links); only positions marked 0xffff compute their
+// hash and read the previous segment's final head table.
+__global__ void __launch_bounds__(256) k_hash_fix2(const LaneDev* __restrict__ lanes,
+                                                   const WorkItem* __restrict__ work, uint16_t* __restrict__ pd,
+                                                   const uint16_t* __restrict__ seg_heads) {
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + HP4_SEG, n);
+  const bool first = s == 0;
+  const uint16_t* prev = seg_heads + (uint64_t)(blockIdx.x - 1) * 32768;  // same lane's previous segment
+  uint16_t* out = pd + L.pbase;
+  const uint8_t* src = L.src;
+  for (uint64_t q0 = s + 8 * threadIdx.x; q0 < e; q0 += 8 * 256) {
+    uint16_t v[8];
+    const bool vec = q0 + 8 <= e && ((reinterpret_cast<uintptr_t>(out + q0) & 15) == 0);
+    if (vec) {
+      *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(out + q0);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] = q0 + k < e ? out[q0 + k] : 0;
+    }
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (v[k] != 0xffff) continue;
+      any = true;
+      const uint64_t q = q0 + k;
+      uint32_t d = 0;
+      if (!first) {
+        const uint32_t h =
+            (((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^ __ldg(src + q + 2)) & 0x7fff;
+        const uint32_t r = prev[h];
+        if (r) {
+          const uint64_t dd = q - ((s - HP4_SEG) + r - 1);
+          d = dd < WSIZE ? (uint32_t)dd : 0;
+        }
+      }
+      v[k] = (uint16_t)d;
+    }
+    if (!any) continue;
+    if (vec) {
+      *reinterpret_cast<uint4*>(out + q0) = *reinterpret_cast<const uint4*>(v);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; k++)
+        if (q0 + k < e) out[q0 + k] = v[k];
+    }
+  }
+}
+
 static int hash_prev_two_phase(Workspace& sortws, Workspace& W, const LaneDev* d_lanes, int nl,
                                const std::vector<uint64_t>& lane_prefix, uint16_t* d_pd, cudaStream_t st) {
   std::vector<WorkItem> work;
@@ -671,8 +724,7 @@ static int hash_prev_two_phase(Workspace& sortws, Workspace& W, const LaneDev* d
     k_hash_prev5<<<grid, HP5_THREADS, HP5_SMEM, st>>>(d_lanes, d_work, (uint32_t)work.size(), d_pd, heads);
   }
   BB_LAUNCH_CHECK();
-  k_hash_fix<<<grid_for(lane_prefix[nl], 256, 16), 256, 0, st>>>(d_lanes, nl, d_lp, d_seg0, lane_prefix[nl], d_pd,
-                                                                  heads);
+  k_hash_fix2<<<(unsigned)work.size(), 256, 0, st>>>(d_lanes, d_work, d_pd, heads);
   BB_LAUNCH_CHECK();
   return BB_OK;
 }
