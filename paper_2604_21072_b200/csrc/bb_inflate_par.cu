@@ -678,8 +678,14 @@ __global__ void __launch_bounds__(ND_THREADS) k_decode_nodes(const PJob* __restr
 constexpr int WD_WARPS = 4;
 __device__ unsigned long long g_wd[8];  // watchdog trips per loop site (debug)
 __device__ unsigned* g_prog;             // debug: progress words in mapped host memory (or null)
+#ifdef BB_PROG_DEBUG  // progress words for hang diagnosis (kept out of the hot loops otherwise)
 #define PROG(d, lane, ph, x) \
   if (g_prog) ((volatile unsigned*)g_prog)[(d) * 32 + (lane)] = ((ph) << 24) | ((unsigned)(x) & 0xffffff)
+#else
+#define PROG(d, lane, ph, x) \
+  do {                       \
+  } while (0)
+#endif
 #define WD_GUARD(site, it, limit, action)        \
   if (++(it) > (limit)) {                        \
     atomicAdd(&g_wd[site], 1ull);                \
@@ -701,7 +707,106 @@ struct DynExtra {
   uint64_t dyn_out, dyn_nm;
 };
 
+// Direct lookup of the next FAST_BITS (literal/length) or FAST_DBITS (distance)
+// stream bits, built per block by the warp from the canonical tables.  Entry:
+// bits 0-3 code length (0: longer code -> the limit-compare decode), bits 4-5
+// kind (0 literal, 1 length, 2 end of block, 3 invalid symbol), bits 6-9 extra
+// bits, bits 16-31 literal byte or length / distance base -- so a symbol costs
+// one shared load, with no divergent __constant__ lookups.
+constexpr int FAST_BITS = 10, FAST_DBITS = 9;
+struct FastT {
+  uint32_t lit[1 << FAST_BITS];
+  uint32_t dist[1 << FAST_DBITS];
+};
+
+template <int CAP, int NB>
+__device__ __forceinline__ void fast_fill(const HTabT<CAP>* t, uint32_t* f, int lane, bool is_dist) {
+  const uint32_t limn = t->lim[NB];
+  for (uint32_t idx = lane; idx < (1u << NB); idx += 32) {
+    const uint32_t w = (__brev(idx) >> (32 - NB)) << (15 - NB);
+    uint32_t e = 0;
+    if ((w | ((1u << (15 - NB)) - 1)) < limn) {
+      int l = 1;
+      for (int k = 1; k < NB; k++) l += (w >= t->lim[k]);
+      const uint32_t sym = t->sym[t->base[l] + (int)(w >> (15 - l))];
+      uint32_t kind, extra = 0, val = 0;
+      if (is_dist) {
+        if (sym < 30) kind = 0, extra = p_dext[sym], val = p_dbase[sym];
+        else kind = 3;
+      } else if (sym < 256) {
+        kind = 0, val = sym;
+      } else if (sym == 256) {
+        kind = 2;
+      } else if (sym < 286) {
+        kind = 1, extra = p_lext[sym - 257], val = p_lbase[sym - 257];
+      } else {
+        kind = 3;
+      }
+      e = (uint32_t)l | (kind << 4) | (extra << 6) | (val << 16);
+    }
+    f[idx] = e;
+  }
+}
+
+__device__ __forceinline__ void fast_build(const Tables* T, FastT* F, int lane) {
+  fast_fill<288, FAST_BITS>(&T->lit, F->lit, lane, false);
+  fast_fill<32, FAST_DBITS>(&T->dist, F->dist, lane, true);
+  __syncwarp();
+}
+
+// dsym with the direct tables (same results and errors as dsym)
+__device__ __forceinline__ int dsymf(BitReader& r, const Tables* T, const FastT* F, const Lims& LL, const Lims& DL,
+                                     uint32_t& len, uint32_t& dist, uint32_t& lit) {
+  r.refill();
+  const uint32_t e = F->lit[(uint32_t)r.hold & ((1u << FAST_BITS) - 1)];
+  if (e & 15) {
+    r.drop(e & 15);
+    if (r.past_end()) return -1;
+    const uint32_t kind = (e >> 4) & 3;
+    if (kind == 0) {
+      lit = e >> 16;
+      len = 1;
+      return 0;
+    }
+    if (kind == 2) return 2;
+    if (kind == 3) return -1;
+    len = (e >> 16) + r.take((e >> 6) & 15);
+  } else {
+    int sym = hdecode(r, &T->lit, LL);
+    if (sym < 0) return -1;
+    if (sym < 256) {
+      lit = (uint32_t)sym;
+      len = 1;
+      return 0;
+    }
+    if (sym == 256) return 2;
+    sym -= 257;
+    if (sym >= 29) return -1;
+    len = p_lbase[sym] + r.take(p_lext[sym]);
+  }
+  r.refill();
+  const uint32_t ed = F->dist[(uint32_t)r.hold & ((1u << FAST_DBITS) - 1)];
+  if (ed & 15) {
+    r.drop(ed & 15);
+    if (r.past_end()) return -1;
+    if (((ed >> 4) & 3) == 3) return -1;
+    dist = (ed >> 16) + r.take((ed >> 6) & 15);
+  } else {
+    int ds = hdecode(r, &T->dist, DL);
+    if (ds < 0 || ds >= 30) return -1;
+    dist = p_dbase[ds] + r.take(p_dext[ds]);
+  }
+  if (r.past_end()) return -1;
+  return 1;
+}
+
+struct EmitSm {
+  FastT F;
+  Tables T;
+};
+
 struct WarpSm {
+  FastT F;
   Tables T;
   uint32_t rpos[32][REC];
   uint32_t rout[32][REC];
@@ -767,6 +872,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
     return;
   }
   __syncwarp();
+  fast_build(&W.T, &W.F, lane);
   Lims LL, DL;
   LL.load(&W.T.lit);
   DL.load(&W.T.dist);
@@ -797,7 +903,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
       nrec++;
     }
     uint32_t len = 0, dist = 0, lit = 0;
-    int t = dsym(r, &W.T, LL, DL, len, dist, lit);
+    int t = dsymf(r, &W.T, &W.F, LL, DL, len, dist, lit);
     if (t < 0) {
       stuck = true;
       err_at = p;
@@ -866,7 +972,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
         }
         uint32_t len = 0, dist = 0, lit = 0;
         const uint64_t p = t;
-        int ty = dsym(q, &W.T, LL, DL, len, dist, lit);
+        int ty = dsymf(q, &W.T, &W.F, LL, DL, len, dist, lit);
         if (ty < 0) {
           real_err = p;
           done = true;
@@ -912,7 +1018,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
       PROG(d, lane, 6, it2);
       uint32_t len = 0, dist = 0, lit = 0;
       const uint64_t p = q.pos;
-      int ty = dsym(q, &W.T, LL, DL, len, dist, lit);
+      int ty = dsymf(q, &W.T, &W.F, LL, DL, len, dist, lit);
       if (ty < 0) {
         bad = true;
         break;
@@ -1007,7 +1113,8 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restri
                                                            const DynExtra* __restrict__ extra,
                                                            Match* __restrict__ matches, uint32_t* __restrict__ fail) {
   extern __shared__ __align__(16) uint8_t smraw[];
-  Tables& T = reinterpret_cast<Tables*>(smraw)[threadIdx.x >> 5];
+  EmitSm& ES = reinterpret_cast<EmitSm*>(smraw)[threadIdx.x >> 5];
+  Tables& T = ES.T;
   const int lane = threadIdx.x & 31;
   const uint32_t j = job_of_chain_block[blockIdx.x];
   const PJob J = jobs[j];
@@ -1023,6 +1130,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restri
     for (uint32_t k = lane; k < sizeof(Tables) / 4; k += 32) dstw[k] = srcw[k];
   }
   __syncwarp();
+  fast_build(&T, &ES.F, lane);
   const LanePlan lp = plans[(uint64_t)d * 32 + lane];
   const uint64_t base = out_off[J.node0 + i];
   Match* mm = matches + J.mbase + m_off[J.node0 + i];
@@ -1039,7 +1147,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restri
     while (r.pos < lp.end) {
       WD_GUARD(3, it3, (1ull << 20), { bad = true; break; })
       uint32_t len = 0, dist = 0, lit = 0;
-      int ty = dsym(r, &T, LL, DL, len, dist, lit);
+      int ty = dsymf(r, &T, &ES.F, LL, DL, len, dist, lit);
       if (ty == 0) {
         J.dst[o++] = (uint8_t)lit;
       } else if (ty == 1) {
@@ -1857,7 +1965,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   // P5
   T.mark("inflate.emit");
   if (!emit_job.empty()) {
-    k_dyn_emit<<<(unsigned)emit_job.size(), 32 * WD_WARPS, sizeof(Tables) * WD_WARPS, st>>>(
+    k_dyn_emit<<<(unsigned)emit_job.size(), 32 * WD_WARPS, sizeof(EmitSm) * WD_WARPS, st>>>(
         d_jobs, d_chains, d_chain_nodes, d_emit_job, d_emit_base, d_nodes, d_out_off, d_m_off, d_dtabs, d_plans,
         d_extra, d_matches, d_fail);
     BB_LAUNCH_CHECK();
