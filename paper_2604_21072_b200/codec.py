@@ -298,7 +298,13 @@ class DeviceCodec:
         self.torch = torch
         self.device = device
         self.L = _lib.load()
-        self.ctx = _lib.context(device)
+        _lib.context(device)
+
+    @property
+    def ctx(self):
+        """The calling thread's C-ABI context (contexts are per host thread), so one
+        DeviceCodec can be driven from several threads, each on its own stream."""
+        return _lib.context(self.device)
 
     def _stream(self, stream=None) -> int:
         s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
