@@ -1706,8 +1706,7 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   __syncthreads();
   const uint32_t* sy = syms + Ld.sym_base + s0;
   uint32_t local = 0;
-  for (uint32_t i = threadIdx.x; i < nsym; i += blockDim.x) {
-    uint32_t v = sy[i];
+  auto count = [&](uint32_t v) {
     if (v & SYM_MATCH) {
       uint32_t lc = v & 0xff, dist = (v >> 8) & 0x7fff;
       local += lc + 3;
@@ -1717,7 +1716,17 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
       local += 1;
       atomicAdd(&h_l[v & 0xff], 1u);
     }
-    if (i == nsym - 1) s_last_len = sym_len(v);
+  };
+  {
+    // four independent loads in flight per thread (the symbol stream comes from DRAM)
+    uint32_t i = threadIdx.x;
+    for (; i + 3 * BK_THREADS < nsym; i += 4 * BK_THREADS) {
+      const uint32_t v0 = __ldg(sy + i), v1 = __ldg(sy + i + BK_THREADS), v2 = __ldg(sy + i + 2 * BK_THREADS),
+                     v3 = __ldg(sy + i + 3 * BK_THREADS);
+      count(v0), count(v1), count(v2), count(v3);
+    }
+    for (; i < nsym; i += BK_THREADS) count(__ldg(sy + i));
+    if (threadIdx.x == 0 && nsym) s_last_len = sym_len(__ldg(sy + nsym - 1));
   }
   // reduce stored length
   for (int o = 16; o; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
@@ -1775,20 +1784,21 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) {
     bc->d[i] = (uint32_t)S.dt.code[i] | ((uint32_t)S.dt.len[i] << 16);
   }
-  // exact sizes from the symbols themselves (forced zero-frequency codes excluded)
-  for (uint32_t i = threadIdx.x; i < nsym; i += blockDim.x) {
-    uint32_t v = sy[i];
-    if (v & SYM_MATCH) {
-      uint32_t lc = v & 0xff, dist = (v >> 8) & 0x7fff;
-      uint32_t code = c_z.length_code[lc];
-      uint32_t dc = d_code(dist);
-      uint32_t x = c_extra_lbits[code] + c_extra_dbits[dc];
-      dsum += S.lt.len[code + 257] + S.dt.len[dc] + x;
-      ssum += c_z.sl_len[code + 257] + 5 + x;
-    } else {
-      dsum += S.lt.len[v & 0xff];
-      ssum += c_z.sl_len[v & 0xff];
-    }
+  // exact sizes from the symbol histograms (the real counts h_l / h_d, so the
+  // frequency-1 nodes build_tree forces into sparse trees are not counted)
+  for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) {
+    const uint32_t f = h_l[i];
+    if (!f) continue;
+    const uint32_t x = i >= 257 ? c_extra_lbits[i - 257] : 0;
+    dsum += (unsigned long long)f * (S.lt.len[i] + x);
+    ssum += (unsigned long long)f * (c_z.sl_len[i] + x);
+  }
+  for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) {
+    const uint32_t f = h_d[i];
+    if (!f) continue;
+    const uint32_t x = c_extra_dbits[i];
+    dsum += (unsigned long long)f * (S.dt.len[i] + x);
+    ssum += (unsigned long long)f * (5 + x);
   }
   for (int o = 16; o; o >>= 1) {
     dsum += __shfl_down_sync(0xffffffffu, dsum, o);
