@@ -713,7 +713,7 @@ struct DynExtra {
 // kind (0 literal, 1 length, 2 end of block, 3 invalid symbol), bits 6-9 extra
 // bits, bits 16-31 literal byte or length / distance base -- so a symbol costs
 // one shared load, with no divergent __constant__ lookups.
-constexpr int FAST_BITS = 10, FAST_DBITS = 9;
+constexpr int FAST_BITS = 9, FAST_DBITS = 8;
 struct FastT {
   uint32_t lit[1 << FAST_BITS];
   uint32_t dist[1 << FAST_DBITS];
@@ -772,7 +772,7 @@ __device__ __forceinline__ int dsymf(BitReader& r, const Tables* T, const FastT*
     if (kind == 3) return -1;
     len = (e >> 16) + r.take((e >> 6) & 15);
   } else {
-    int sym = hdecode(r, &T->lit, LL);
+    int sym = hdecode(r, &T->lit);  // long code: limits from shared memory
     if (sym < 0) return -1;
     if (sym < 256) {
       lit = (uint32_t)sym;
@@ -792,7 +792,7 @@ __device__ __forceinline__ int dsymf(BitReader& r, const Tables* T, const FastT*
     if (((ed >> 4) & 3) == 3) return -1;
     dist = (ed >> 16) + r.take((ed >> 6) & 15);
   } else {
-    int ds = hdecode(r, &T->dist, DL);
+    int ds = hdecode(r, &T->dist);
     if (ds < 0 || ds >= 30) return -1;
     dist = p_dbase[ds] + r.take(p_dext[ds]);
   }
@@ -809,8 +809,8 @@ struct WarpSm {
   FastT F;
   Tables T;
   uint32_t rpos[32][REC];
-  uint32_t rout[32][REC];
-  uint32_t rnm[32][REC];
+  uint16_t rout[32][REC];  // output bytes before record j of the lane (<= REC * 258)
+  uint16_t rnm[32][REC];   // matches before record j
 };
 
 // one lit/len symbol (+ distance): 0 literal, 1 match, 2 end of block, -1 invalid
@@ -834,7 +834,7 @@ __device__ __forceinline__ int dsym(BitReader& r, const Tables* T, const Lims& L
   return 1;
 }
 
-__global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restrict__ jobs,
+__global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __restrict__ jobs,
                                                            const uint32_t* __restrict__ node_job,
                                                            const uint32_t* __restrict__ dyn_nodes, uint32_t ndyn_total,
                                                            Node* __restrict__ nodes, Tables* __restrict__ tabs,
@@ -898,8 +898,8 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_scan(const PJob* __restri
     const uint64_t p = r.pos;
     if (nrec < REC) {
       W.rpos[lane][nrec] = (uint32_t)(p - d0);
-      W.rout[lane][nrec] = (uint32_t)out;
-      W.rnm[lane][nrec] = (uint32_t)nm;
+      W.rout[lane][nrec] = (uint16_t)out;
+      W.rnm[lane][nrec] = (uint16_t)nm;
       nrec++;
     }
     uint32_t len = 0, dist = 0, lit = 0;
