@@ -1094,7 +1094,13 @@ __device__ __forceinline__ uint32_t pf_pick(const uint32_t (&c)[B], int t) {
   return v;
 }
 
-constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;  // sentinel word is 0: its byte_perm low half never equals 0xffff
+constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;
+#ifndef PF_B1
+#define PF_B1 4  // chain steps per batch within the first 32 (budget-32 snapshot)
+#endif
+#ifndef PF_B2
+#define PF_B2 16  // chain steps per batch for candidates 33..128
+#endif  // sentinel word is 0: its byte_perm low half never equals 0xffff
 
 __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __restrict__ lanes,
                                                             const WorkItem* __restrict__ work,
@@ -1166,7 +1172,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
           const int t = __ffs(mask) - 1;
           mask &= mask - 1;
           const uint32_t c = pf_pick(cand, t);
-          if ((((w32[c] ^ wp) | (w32[c + best - 1] ^ w32[ip1 + best - 1])) & 0xffff0000u) != 0) continue;
+          // re-test only if best grew in this flush (else it is the test the step already made)
+          if (improved && (((w32[c] ^ wp) | (w32[c + best - 1] ^ w32[ip1 + best - 1])) & 0xffff0000u) != 0)
+            continue;
           uint32_t len = 2;
           while (len < maxl) {
             const uint32_t x = (w32[c + len] ^ w32[ip1 + len]) >> 16;
@@ -1193,14 +1201,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
         }
       }
     };
-    for (int cnt = 0; cnt < 32; cnt += 4) {
+    for (int cnt = 0; cnt < 32; cnt += PF_B1) {
       if (!__any_sync(0xffffffffu, ic1 != 0)) break;
-      batch(std::integral_constant<int, 4>());
+      batch(std::integral_constant<int, PF_B1>());
     }
     const uint32_t r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
-    for (int cnt = 32; cnt < (int)MAX_CHAIN; cnt += 8) {
+    for (int cnt = 32; cnt < (int)MAX_CHAIN; cnt += PF_B2) {
       if (!__any_sync(0xffffffffu, ic1 != 0)) break;
-      batch(std::integral_constant<int, 8>());
+      batch(std::integral_constant<int, PF_B2>());
     }
     if (p < e) prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, live ? r32 | flag : 0);
   }

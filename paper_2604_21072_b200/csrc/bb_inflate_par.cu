@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(ND_THREADS) k_decode_nodes(const PJob* __restr
 // starts, and the true decode entering a chunk (the previous lane's exit) is
 // advanced only until it lands on one of them.  Pass 2 (k_dyn_emit) then
 // decodes every lane's exact sub-range again, writing its output.
-constexpr int WD_WARPS = 4;
+constexpr int WD_WARPS = 2;
 __device__ unsigned long long g_wd[8];  // watchdog trips per loop site (debug)
 __device__ unsigned* g_prog;             // debug: progress words in mapped host memory (or null)
 #ifdef BB_PROG_DEBUG  // progress words for hang diagnosis (kept out of the hot loops otherwise)
