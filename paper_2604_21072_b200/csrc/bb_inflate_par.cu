@@ -27,6 +27,7 @@
 //                     the window; the rest are resolved window by window in order
 //                     (k_resolve_ext: one gather per window)
 //   P7 Adler-32 check, size check
+#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -1570,6 +1571,131 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
   if (threadIdx.x == 0) ext_cnt[blockIdx.x] = s_cnt;
 }
 
+// P6 (current): the pointer jumping runs over RS_CL consecutive windows of a
+// lane at once -- a thread-block cluster whose CTAs each hold one 32 KiB window
+// in shared memory and read their neighbours' entries through distributed
+// shared memory.  Copy chains are long (literals are rare in exponent planes and
+// each hop goes back up to 32 KiB), so a 4x larger window leaves far fewer bytes
+// (and shorter chains) to k_resolve_chase.  Entries: RESOLVED | byte, or the
+// source as an offset from (cluster base - 65536); < 65536 = before the cluster.
+namespace cg = cooperative_groups;
+constexpr int RS_CL = 4;
+
+__global__ void __cluster_dims__(RS_CL, 1, 1) __launch_bounds__(RS_THREADS)
+    k_resolve_cluster(const PJob* __restrict__ jobs, const uint2* __restrict__ cl_map,
+                      const uint64_t* __restrict__ out_total, uint32_t* __restrict__ fail,
+                      const Match* __restrict__ matches, ExtEntry* __restrict__ ext, uint32_t* __restrict__ ext_cnt,
+                      uint32_t* __restrict__ extp, uint8_t* __restrict__ wflag) {
+  extern __shared__ uint32_t ent[];
+  __shared__ int s_corrupt, s_anyv[3];
+  __shared__ uint32_t s_cnt;
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  const uint2 cm = cl_map[blockIdx.x / RS_CL];  // (job, first window of the cluster)
+  const uint32_t j = cm.x;
+  const PJob J = jobs[j];
+  const uint32_t w = cm.y + rank;
+  const bool failed = fail[j] != 0;
+  const uint64_t total = out_total[2 * j];
+  const uint64_t CB = (uint64_t)cm.y * SUB;  // cluster base position
+  const uint64_t S = (uint64_t)w * SUB;
+  const uint32_t Wn = (!failed && w < J.nsub && S < total) ? (uint32_t)min((uint64_t)SUB, total - S) : 0;
+  const uint32_t g = J.sub0 + w;  // global window index (valid only if w < nsub)
+  const uint64_t nm = out_total[2 * j + 1];
+  const Match* M = matches + J.mbase;
+  uint64_t m0 = 0;
+  bool has_m = false;
+  if (Wn) {
+    m0 = first_match_after(M, nm, S);
+    has_m = m0 < nm && M[m0].dst < S + Wn;
+  }
+  if (threadIdx.x == 0) {
+    s_corrupt = 0;
+    s_cnt = 0;
+    s_anyv[0] = 0;
+    if (w < J.nsub) wflag[g] = has_m ? 1 : 0;
+  }
+  // a cluster none of whose windows holds a match (e.g. stored mantissa planes) is done
+  cl.sync();
+  if (threadIdx.x == 0 && has_m) atomicOr(cl.map_shared_rank(&s_anyv[0], 0), 1);
+  cl.sync();
+  if (!*cl.map_shared_rank(&s_anyv[0], 0)) {
+    if (threadIdx.x == 0 && w < J.nsub) ext_cnt[g] = 0;
+    cl.sync();  // rank 0's flag is read by all before anyone exits
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < SUB; i += blockDim.x) ent[i] = RESOLVED | (i < Wn ? J.dst[S + i] : 0u);
+  __syncthreads();
+  if (has_m) {
+    for (uint64_t k = m0 + threadIdx.x; k < nm && M[k].dst < S + Wn; k += blockDim.x) {
+      const Match mt = M[k];
+      if (mt.dist == 0 || mt.dist > mt.dst || mt.len < 3 || mt.len > 258) {
+        s_corrupt = 1;
+        continue;
+      }
+      const uint64_t a = max((uint64_t)mt.dst, S), b = min((uint64_t)mt.dst + mt.len, S + Wn);
+      for (uint64_t x = a; x < b; x++) ent[x - S] = (uint32_t)(x - mt.dist + 65536 - CB);
+    }
+  }
+  cl.sync();
+  // pointer jumping over the cluster's windows (reads of neighbours may see an
+  // older or newer entry of the same chain: both are valid, pointers only move
+  // toward their roots).  Each thread keeps a bit mask of its still-unresolved
+  // entries (entry threadIdx.x + 1024 k -> bit k); the cluster-wide "anything
+  // changed" flag is triple-buffered in rank 0's shared memory so one cluster
+  // barrier per round suffices (flag r+1 is cleared in round r, when every CTA
+  // has long finished reading flag r-2, the same slot).
+  uint32_t pend = 0;
+  for (uint32_t k = 0; k < SUB / RS_THREADS; k++) {
+    const uint32_t i = threadIdx.x + k * RS_THREADS;
+    if (i < Wn && !(ent[i] & RESOLVED) && ent[i] >= 65536) pend |= 1u << k;
+  }
+  if (threadIdx.x < 3) s_anyv[threadIdx.x] = 0;
+  cl.sync();
+  int rounds = 0;
+  for (;;) {
+    const int slot = rounds % 3;
+    if (rank == 0 && threadIdx.x == 0) s_anyv[(rounds + 1) % 3] = 0;
+    uint32_t next = 0;
+    for (uint32_t m = pend; m; m &= m - 1) {
+      const uint32_t k = __ffs(m) - 1;
+      const uint32_t i = threadIdx.x + k * RS_THREADS;
+      const uint32_t e = ent[i];
+      const uint32_t idx = e - 65536;
+      const unsigned r = idx / SUB;
+      const uint32_t o = idx % SUB;
+      const uint32_t t = r == rank ? ent[o] : *cl.map_shared_rank(ent + o, r);
+      ent[i] = t;
+      if (!(t & RESOLVED) && t >= 65536) next |= 1u << k;
+    }
+    const int ch = __syncthreads_or(pend != 0);
+    pend = next;
+    if (threadIdx.x == 0 && ch) atomicOr(cl.map_shared_rank(&s_anyv[slot], 0), 1);
+    cl.sync();
+    const int any = *cl.map_shared_rank(&s_anyv[slot], 0);
+    if (!any || ++rounds > 48) break;
+  }
+  if (Wn && (s_corrupt || rounds > 48)) {
+    if (threadIdx.x == 0) atomicExch(&fail[j], 1u);
+  } else if (has_m) {
+    for (uint32_t i = threadIdx.x; i < Wn; i += blockDim.x) {
+      const uint32_t e = ent[i];
+      if (e & RESOLVED) {
+        J.dst[S + i] = (uint8_t)e;
+        extp[J.xbase + S + i] = 0xFFFFFFFFu;
+      } else {
+        const uint32_t k = atomicAdd(&s_cnt, 1u);
+        const uint32_t src = (uint32_t)(CB + e - 65536);
+        ext[(uint64_t)g * SUB + k] = ExtEntry{(uint32_t)(S + i), src};
+        extp[J.xbase + S + i] = src;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && w < J.nsub) ext_cnt[g] = has_m && !s_corrupt ? s_cnt : 0;
+  cl.sync();  // no CTA may exit while a neighbour can still read its shared memory
+}
+
 // Every byte left unresolved by its window points to an earlier byte; chase
 // the pointers (read-only map) to a byte its own window resolved.  Fully
 // parallel over all windows of all lanes.
@@ -1715,6 +1841,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_emit_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(sizeof(WarpSm) * WD_WARPS)));
     attr = true;
@@ -1755,7 +1882,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
                 2 * al(4 * swords) + al(4 * sub_job.size() + 4) + al(4 * chunk_job.size() + 4) + al(4 * nj) +
                 al(16 * chunk_job.size() + 16) + al(sizeof(Match) * mtot) + al(sizeof(ExtEntry) * (uint64_t)subs * SUB) +
                 al(4 * subs + 4) + al(subs + 4) + al(4 * xtot + 4) + al(8 * (ntot_bytes / 2 + 4096)) + 256 + al(4 * nj) * 6 + al(16 * nj) * 4 + al(sizeof(Chain) * nj) +
-                al(sizeof(Tables) * nj) + 65536;
+                al(sizeof(Tables) * nj) + al(8 * ((uint64_t)subs + nj + 1)) + 65536;
   int rc = P->ws.reserve(need);
   if (rc) return rc;
   Workspace& W = P->ws;
@@ -1774,6 +1901,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   uint32_t* d_ext_cnt = W.take<uint32_t>(subs + 1);
   uint32_t* d_extp = W.take<uint32_t>(xtot + 1);
   uint8_t* d_wflag = W.take<uint8_t>(subs + 1);
+  uint2* d_clm = W.take<uint2>(subs + nj + 1);  // (job, first window) per resolution cluster
   const uint64_t surv_cap = find_dynamic ? ntot_bytes / 2 + 4096 : 1;
   uint64_t* d_surv = W.take<uint64_t>(surv_cap);
   unsigned long long* d_surv_cnt = W.take<unsigned long long>(1);
@@ -1981,8 +2109,20 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   // P6
   T.mark("inflate.resolve");
   if (!sub_job.empty()) {
-    k_resolve_local<<<(unsigned)sub_job.size(), RS_THREADS, SUB * 4, st>>>(d_jobs, d_sub_job, d_out_total, d_fail,
-                                                                     d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
+    // stored-only pass (A): windows rarely hold matches, per-window CTAs exit at once;
+    // the dynamic pass (B) resolves copy chains over clusters of windows
+    static const bool single = getenv("BB_RESOLVE_SINGLE") != nullptr;
+    if (single || !find_dynamic) {
+      k_resolve_local<<<(unsigned)sub_job.size(), RS_THREADS, SUB * 4, st>>>(d_jobs, d_sub_job, d_out_total, d_fail,
+                                                                       d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
+    } else {
+      std::vector<uint2> clm;
+      for (int i = 0; i < nj; i++)
+        for (uint32_t w0 = 0; w0 < J[i].nsub; w0 += RS_CL) clm.push_back(make_uint2((uint32_t)i, w0));
+      BB_CUDA_TRY(cudaMemcpyAsync(d_clm, clm.data(), sizeof(uint2) * clm.size(), cudaMemcpyHostToDevice, st));
+      k_resolve_cluster<<<(unsigned)(clm.size() * RS_CL), RS_THREADS, SUB * 4, st>>>(
+          d_jobs, d_clm, d_out_total, d_fail, d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
+    }
     BB_LAUNCH_CHECK();
     k_resolve_chase<<<(unsigned)sub_job.size(), 256, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
                                                              d_wflag);
