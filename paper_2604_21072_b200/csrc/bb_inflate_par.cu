@@ -1575,11 +1575,11 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
 // lane at once -- a thread-block cluster whose CTAs each hold one 32 KiB window
 // in shared memory and read their neighbours' entries through distributed
 // shared memory.  Copy chains are long (literals are rare in exponent planes and
-// each hop goes back up to 32 KiB), so a 4x larger window leaves far fewer bytes
+// each hop goes back up to 32 KiB), so a larger window leaves fewer bytes
 // (and shorter chains) to k_resolve_chase.  Entries: RESOLVED | byte, or the
 // source as an offset from (cluster base - 65536); < 65536 = before the cluster.
 namespace cg = cooperative_groups;
-constexpr int RS_CL = 4;
+constexpr int RS_CL = 2;
 
 __global__ void __cluster_dims__(RS_CL, 1, 1) __launch_bounds__(RS_THREADS)
     k_resolve_cluster(const PJob* __restrict__ jobs, const uint2* __restrict__ cl_map,
