@@ -801,6 +801,100 @@ __device__ __forceinline__ int dsymf(BitReader& r, const Tables* T, const FastT*
   return 1;
 }
 
+// Word-refill bit reader for the hot decode loops: a 64-bit window refilled
+// 32 bits at a time from aligned words (one 32-bit load per refill instead of
+// peek64's unaligned pair), positions counted as 32-bit offsets from the range
+// start.  Words past the stream end read as zero (the callers' range and count
+// checks reject any decode that ran into them).
+struct WordReader {
+  const uint32_t* w;  // aligned words covering the stream
+  uint32_t wi, wend;  // next word to load, words available
+  uint64_t hold;
+  int bits;
+  uint32_t used;  // bits consumed since init
+  __device__ __forceinline__ uint32_t word(uint32_t k) const { return k < wend ? __ldg(w + k) : 0u; }
+  __device__ __forceinline__ void init(const uint8_t* p, uint64_t n, uint64_t bitpos) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint64_t abit = bitpos + 8 * (a & 3);  // bit position in the aligned frame
+    wend = (uint32_t)((n + (a & 3) + 3) / 4);
+    const uint32_t k = (uint32_t)(abit >> 5), sh = (uint32_t)(abit & 31);
+    hold = ((uint64_t)word(k) | ((uint64_t)word(k + 1) << 32)) >> sh;
+    bits = 64 - (int)sh;
+    wi = k + 2;
+    used = 0;
+  }
+  __device__ __forceinline__ void refill() {
+    if (bits <= 32) {
+      hold |= (uint64_t)word(wi++) << bits;
+      bits += 32;
+    }
+  }
+  __device__ __forceinline__ void drop(uint32_t k) {
+    hold >>= k;
+    bits -= (int)k;
+    used += k;
+  }
+  __device__ __forceinline__ uint32_t take(uint32_t k) {  // k <= 13, bits >= 13 guaranteed by refill
+    const uint32_t v = (uint32_t)hold & ((1u << k) - 1);
+    drop(k);
+    return v;
+  }
+};
+
+// limit-compare decode of a code longer than the direct table (limits from shared memory)
+template <int CAP>
+__device__ __forceinline__ int wdecode_slow(WordReader& r, const HTabT<CAP>* t) {
+  const uint32_t x = __brev((uint32_t)r.hold) >> 17;
+  int l = 1;
+#pragma unroll
+  for (int k = 1; k < 16; k++) l += (x >= t->lim[k]);
+  if (l > 15) return -1;
+  const int s = t->sym[t->base[l] + (int)(x >> (15 - l))];
+  r.drop((uint32_t)l);
+  return s;
+}
+
+// one literal/length (+ distance) symbol: 0 literal, 1 match, 2 end of block, -1 invalid
+__device__ __forceinline__ int wsym(WordReader& r, const Tables* T, const FastT* F, uint32_t& len, uint32_t& dist,
+                                    uint32_t& lit) {
+  r.refill();
+  const uint32_t e = F->lit[(uint32_t)r.hold & ((1u << FAST_BITS) - 1)];
+  uint32_t kind, base, extra;
+  if (e & 15) {
+    r.drop(e & 15);
+    kind = (e >> 4) & 3, base = e >> 16, extra = (e >> 6) & 15;
+  } else {
+    const int sym = wdecode_slow(r, &T->lit);
+    if (sym < 0) return -1;
+    if (sym < 256) kind = 0, base = (uint32_t)sym, extra = 0;
+    else if (sym == 256) kind = 2, base = 0, extra = 0;
+    else if (sym < 286) kind = 1, base = p_lbase[sym - 257], extra = p_lext[sym - 257];
+    else return -1;
+  }
+  if (kind == 0) {
+    lit = base;
+    len = 1;
+    return 0;
+  }
+  if (kind != 1) return kind == 2 ? 2 : -1;
+  len = base + r.take(extra);  // <= 15 + 5 bits used since the refill: >= 13 left
+  r.refill();
+  const uint32_t ed = F->dist[(uint32_t)r.hold & ((1u << FAST_DBITS) - 1)];
+  if (ed & 15) {
+    r.drop(ed & 15);
+    if (((ed >> 4) & 3) == 3) return -1;
+    r.refill();
+    dist = (ed >> 16) + r.take((ed >> 6) & 15);
+  } else {
+    const int ds = wdecode_slow(r, &T->dist);
+    if (ds < 0 || ds >= 30) return -1;
+    r.refill();
+    dist = p_dbase[ds] + r.take(p_dext[ds]);
+  }
+  return 1;
+}
+
 struct EmitSm {
   FastT F;
   Tables T;
@@ -884,7 +978,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __res
   const uint64_t span = E - d0;
   const uint64_t s_k = d0 + span * lane / 32, s_n = d0 + span * (lane + 1) / 32;
   // round 1
-  BitReader r;
+  WordReader r;
   r.init(J.src, J.n, s_k);
   uint64_t out = 0, nm = 0;
   int nrec = 0;
@@ -893,10 +987,10 @@ __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __res
   uint64_t eob_at = NONE64, eob_end = 0, eob_out = 0, eob_nm = 0, err_at = NONE64;
   uint64_t eob2_at = NONE64, eob2_end = 0, eob2_out = 0, eob2_nm = 0;
   uint64_t it0 = 0;
-  while (r.pos < s_n) {
-    WD_GUARD(0, it0, (1ull << 16), { stuck = true; err_at = r.pos; break; })
+  while (s_k + r.used < s_n) {
+    WD_GUARD(0, it0, (1ull << 16), { stuck = true; err_at = s_k + r.used; break; })
     PROG(d, lane, 2, it0);
-    const uint64_t p = r.pos;
+    const uint64_t p = s_k + r.used;
     if (nrec < REC) {
       W.rpos[lane][nrec] = (uint32_t)(p - d0);
       W.rout[lane][nrec] = (uint16_t)out;
@@ -904,21 +998,22 @@ __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __res
       nrec++;
     }
     uint32_t len = 0, dist = 0, lit = 0;
-    int t = dsymf(r, &W.T, &W.F, LL, DL, len, dist, lit);
+    int t = wsym(r, &W.T, &W.F, len, dist, lit);
     if (t < 0) {
       stuck = true;
       err_at = p;
       break;
     }
     if (t == 2) {
-      if (eob_at == NONE64) eob_at = p, eob_end = r.pos, eob_out = out, eob_nm = nm;
-      else if (eob2_at == NONE64) eob2_at = p, eob2_end = r.pos, eob2_out = out, eob2_nm = nm;
+      const uint64_t pe = s_k + r.used;
+      if (eob_at == NONE64) eob_at = p, eob_end = pe, eob_out = out, eob_nm = nm;
+      else if (eob2_at == NONE64) eob2_at = p, eob2_end = pe, eob2_out = out, eob2_nm = nm;
       continue;
     }
     out += len;
     nm += (t == 1);
   }
-  const uint64_t f = stuck ? NONE64 : r.pos;
+  const uint64_t f = stuck ? NONE64 : s_k + r.used;
   __syncwarp();
   // fix-up rounds: the true decode enters lane k's chunk at F_{k-1}
   uint64_t F = f, cnt_out = out, cnt_nm = nm;       // corrected results (lane 0 is exact)
@@ -943,8 +1038,9 @@ __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __res
       bool done = false;
       real_eob = NONE64;
       real_err = NONE64;
-      BitReader q;
+      WordReader q;
       q.init(J.src, J.n, t);
+      const uint64_t q0 = t;
       uint64_t it1 = 0;
       while (t < s_n) {
         WD_GUARD(1, it1, (1ull << 16), { real_err = t; done = true; break; })
@@ -973,7 +1069,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __res
         }
         uint32_t len = 0, dist = 0, lit = 0;
         const uint64_t p = t;
-        int ty = dsymf(q, &W.T, &W.F, LL, DL, len, dist, lit);
+        int ty = wsym(q, &W.T, &W.F, len, dist, lit);
         if (ty < 0) {
           real_err = p;
           done = true;
@@ -981,18 +1077,18 @@ __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __res
         }
         if (ty == 2) {
           real_eob = p;
-          real_eob_end = q.pos;
+          real_eob_end = q0 + q.used;
           ev_out = o;
           ev_nm = m;
           cnt_out = o;
           cnt_nm = m;
-          F = q.pos;
+          F = q0 + q.used;
           done = true;
           break;
         }
         o += len;
         m += (ty == 1);
-        t = q.pos;
+        t = q0 + q.used;
       }
       if (!done) {
         F = t;
@@ -1011,22 +1107,26 @@ __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __res
   // no end-of-block inside the estimate: the last lane keeps decoding
   uint64_t tail_end = 0;
   if (!evm && lane == 31) {
-    BitReader q;
+    WordReader q;
     q.init(J.src, J.n, F);
     uint64_t it2 = 0;
     for (;;) {
       WD_GUARD(2, it2, (1ull << 20), { bad = true; break; })
       PROG(d, lane, 6, it2);
       uint32_t len = 0, dist = 0, lit = 0;
-      const uint64_t p = q.pos;
-      int ty = dsymf(q, &W.T, &W.F, LL, DL, len, dist, lit);
+      const uint64_t p = F + q.used;
+      if (p > 8 * J.n) {  // ran off the stream
+        bad = true;
+        break;
+      }
+      int ty = wsym(q, &W.T, &W.F, len, dist, lit);
       if (ty < 0) {
         bad = true;
         break;
       }
       if (ty == 2) {
         real_eob = p;
-        real_eob_end = q.pos;
+        real_eob_end = F + q.used;
         break;
       }
       lane_out += len;
@@ -1139,18 +1239,19 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restri
   LL.load(&T.lit);
   DL.load(&T.dist);
   bool bad = false;
-  if (lp.end > lp.begin) {
-    BitReader r;
+  if (lp.end > lp.begin && lp.end - lp.begin < (1ull << 31)) {
+    WordReader r;
     r.init(J.src, J.n, lp.begin);
+    const uint32_t span = (uint32_t)(lp.end - lp.begin);
+    uint8_t* dst = J.dst;
     uint64_t o = base + lp.out_off;
     uint32_t m = lp.m_off;
-    uint64_t it3 = 0;
-    while (r.pos < lp.end) {
-      WD_GUARD(3, it3, (1ull << 20), { bad = true; break; })
+    // every symbol consumes >= 1 bit, so the loop ends within span iterations
+    while (r.used < span) {
       uint32_t len = 0, dist = 0, lit = 0;
-      int ty = dsymf(r, &T, &ES.F, LL, DL, len, dist, lit);
+      const int ty = wsym(r, &T, &ES.F, len, dist, lit);
       if (ty == 0) {
-        J.dst[o++] = (uint8_t)lit;
+        dst[o++] = (uint8_t)lit;
       } else if (ty == 1) {
         if (dist > o) {
           bad = true;
@@ -1163,8 +1264,8 @@ __global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restri
         break;
       }
     }
-    if (r.pos != lp.end || o - (base + lp.out_off) != lp.out_cnt || m - lp.m_off != lp.m_cnt) bad = true;
-  } else if (lp.out_cnt || lp.m_cnt) {
+    if (r.used != span || o - (base + lp.out_off) != lp.out_cnt || m - lp.m_off != lp.m_cnt) bad = true;
+  } else if (lp.end > lp.begin || lp.out_cnt || lp.m_cnt) {
     bad = true;
   }
   const DynExtra ex = extra[d];
