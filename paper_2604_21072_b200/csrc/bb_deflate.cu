@@ -8,10 +8,10 @@
 // byte-for-byte against libz.so.1.3 (tests/test_oracle.py).
 //
 // Pipeline over all lanes of a call (lanes = byte planes of every tensor):
-//   K3 k_hash_prev    prev-same-hash distance per position (zlib's head/prev
-//                     chains, which are parse-independent: every position with
+//   K3 k_hash_prev6   prev-same-hash distance per position (zlib's head/prev
+//      k_hash_fix2    chains, which are parse-independent: every position with
 //                     3 bytes of lookahead is inserted, in order)
-//   K4 k_profile      longest_match() for every position: first maximum over the
+//   K4 k_profile3     longest_match() for every position: first maximum over the
 //                     hash chain truncated at nice_match, after 32 and after 128
 //                     candidates (the two chain budgets deflate_slow can use)
 //   K5 k_parse_spec   deflate_slow's lazy-match state machine, one thread per
@@ -29,8 +29,6 @@
 //   K7 k_emit         parallel bit packing of every block into the container
 //      k_adler*       Adler-32 (chunk sums + ordered combine), zlib header/trailer,
 //      k_finalize     BBC1 header
-#include <cub/block/block_radix_sort.cuh>
-#include <cub/device/device_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -206,322 +204,19 @@ __device__ __forceinline__ void hp_load_tile(const uint8_t* src, uint64_t n, uin
     if (c + 128 + t < n) x |= (uint32_t)__ldg(src + c + 128 + t) << (8 * t);
 }
 
-__device__ __forceinline__ uint32_t hp_byte(uint32_t w, uint32_t x, uint32_t i) {
-  // byte i (0..131) of the current tile
-  uint32_t v = __shfl_sync(0xffffffffu, w, (i >> 2) & 31);
-  if (i >= 128) v = x;
-  return (v >> (8 * (i & 3))) & 0xff;
-}
-
-__global__ void __launch_bounds__(32) k_hash_prev(const LaneDev* __restrict__ lanes,
-                                                  const WorkItem* __restrict__ work,
-                                                  uint16_t* __restrict__ pd) {
-  extern __shared__ uint16_t head[];  // 32768 entries: relative position + 1
-  const WorkItem w = work[blockIdx.x];
-  const LaneDev L = lanes[w.lane];
-  const uint64_t n = L.n;
-  const uint64_t s = w.start;
-  const uint64_t e = umin64(s + HP_SEG, n);
-  const uint64_t base = s > WSIZE ? s - WSIZE : 0;
-  const int lane = threadIdx.x;
-  uint4* h4 = reinterpret_cast<uint4*>(head);
-  for (int i = lane; i < 32768 * 2 / 16; i += 32) h4[i] = make_uint4(0, 0, 0, 0);
-  __syncwarp();
-  const uint8_t* src = L.src;
-  uint16_t* out = pd + L.pbase;
-  uint32_t wc, xc;
-  hp_load_tile(src, n, base, lane, wc, xc);
-  for (uint64_t c = base; c < e; c += 128) {
-    uint32_t wn = 0, xn = 0;
-    if (c + 128 < e) hp_load_tile(src, n, c + 128, lane, wn, xn);  // prefetch the next tile
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint32_t i = 32 * k + lane;
-      const uint64_t q = c + i;
-      const uint32_t b0 = hp_byte(wc, xc, i), b1 = hp_byte(wc, xc, i + 1), b2 = hp_byte(wc, xc, i + 2);
-      const bool valid = q < e && q + MIN_MATCH <= n;
-      uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
-      unsigned peers = __match_any_sync(0xffffffffu, h);
-      unsigned lower = peers & ((1u << lane) - 1);
-      uint32_t d = 0;
-      if (valid) {
-        if (lower) {
-          d = lane - (31 - __clz(lower));
-        } else {
-          uint32_t r = head[h];
-          if (r) {
-            uint64_t dd = q - (base + r - 1);
-            d = dd < WSIZE ? (uint32_t)dd : 0;
-          }
-        }
-      }
-      __syncwarp();
-      if (valid && (peers >> lane) == 1u) head[h] = (uint16_t)(q - base + 1);
-      __syncwarp();
-      if (q >= s && q < e) out[q] = (uint16_t)d;
-    }
-    wc = wn;
-    xc = xn;
-  }
-}
-
-// K3 (warp scan): one warp per HP_SEG positions with a 64 KiB u16 head table
-// (three CTAs per SM).  History: scanned newest-first, a hash's first (= most
-// recent) occurrence claims its head.  Segment: scanned oldest-first, 32
-// positions per step; __match_any_sync orders same-hash lanes.  Bytes come in
-// 128-position register tiles prefetched one step ahead.
-__global__ void __launch_bounds__(32) k_hash_prev3(const LaneDev* __restrict__ lanes,
-                                                   const WorkItem* __restrict__ work, uint16_t* __restrict__ pd) {
-  extern __shared__ uint16_t hp3_head[];  // relative position + 1 (0 = none)
-  const WorkItem w = work[blockIdx.x];
-  const LaneDev L = lanes[w.lane];
-  const uint64_t n = L.n;
-  const uint64_t s = w.start;
-  const uint64_t e = umin64(s + HP_SEG, n);
-  const uint64_t base = s > WSIZE ? s - WSIZE : 0;
-  const int lane = threadIdx.x;
-  uint16_t* head = hp3_head;
-  uint4* h4 = reinterpret_cast<uint4*>(head);
-  for (int i = lane; i < 32768 * 2 / 16; i += 32) h4[i] = make_uint4(0, 0, 0, 0);
-  __syncwarp();
-  const uint8_t* src = L.src;
-  // history, newest first: the highest lane of a group claims an unset head
-  for (uint64_t top = s; top > base;) {
-    const uint64_t c = top > base + 32 ? top - 32 : base;
-    const uint64_t q = c + lane;
-    const bool valid = q < top && q + MIN_MATCH <= n;
-    uint32_t h = 0x10000u + lane;
-    if (valid) h = (((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^ __ldg(src + q + 2)) & 0x7fff;
-    const unsigned peers = __match_any_sync(0xffffffffu, h);
-    if (valid && (peers >> lane) == 1u && head[h] == 0) head[h] = (uint16_t)(q - base + 1);
-    __syncwarp();
-    top = c;
-  }
-  uint16_t* out = pd + L.pbase;
-  uint32_t wc, xc;
-  hp_load_tile(src, n, s, lane, wc, xc);
-  for (uint64_t c = s; c < e; c += 128) {
-    uint32_t wn = 0, xn = 0;
-    if (c + 128 < e) hp_load_tile(src, n, c + 128, lane, wn, xn);
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint32_t i = 32 * k + lane;
-      const uint64_t q = c + i;
-      const uint32_t b0 = hp_byte(wc, xc, i), b1 = hp_byte(wc, xc, i + 1), b2 = hp_byte(wc, xc, i + 2);
-      const bool valid = q < e && q + MIN_MATCH <= n;
-      const uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, h);
-      const unsigned lower = peers & ((1u << lane) - 1);
-      uint32_t d = 0;
-      if (valid) {
-        if (lower) {
-          d = lane - (31 - __clz(lower));
-        } else {
-          const uint32_t r = head[h];
-          if (r) {
-            const uint64_t dd = q - (base + r - 1);
-            d = dd < WSIZE ? (uint32_t)dd : 0;
-          }
-        }
-      }
-      __syncwarp();
-      if (valid && (peers >> lane) == 1u) head[h] = (uint16_t)(q - base + 1);
-      __syncwarp();
-      if (q < e) out[q] = (uint16_t)d;
-    }
-    wc = wn;
-    xc = xn;
-  }
-}
-
-// K3 (two-phase warp scan, current): the segments are independent.
-//   k_hash_prev4: one warp per 32 Ki-position segment scans it in order with an
-//     empty 64 KiB u16 head table; positions whose hash has not yet been seen in
-//     the segment get 0xffff ("look in the previous segment"), and the final
-//     table (last occurrence of every hash in the segment) is stored.
-//   k_hash_fix: those positions read the previous segment's table.
-// No history pass: each position is scanned once.
+// K3 (two-phase warp scan): the segments are independent.
+//   k_hash_prev6: one warp per 32 Ki-position segment scans it in order with an
+//     empty 64 KiB u16 head table, 128 positions per tile (__match_any_sync
+//     orders same-hash lanes), bytes prefetched HP6_D tiles ahead into registers
+//     so the serial head-table chain does not also wait on DRAM; positions whose
+//     hash has not yet been seen in the segment get 0xffff ("look in the
+//     previous segment"), and the final table (last occurrence of every hash in
+//     the segment) is stored.
+//   k_hash_fix2: those positions read the previous segment's table.
+// No history pass: each position is scanned once.  (Measured alternatives --
+// one warp per 1024 positions with a block radix sort, a block-parallel scan with
+// per-hash warp masks, a device-wide key sort -- were slower; see profiles/.)
 constexpr uint32_t HP4_SEG = 32768;
-
-__global__ void __launch_bounds__(32) k_hash_prev4(const LaneDev* __restrict__ lanes,
-                                                   const WorkItem* __restrict__ work, uint16_t* __restrict__ pd,
-                                                   uint16_t* __restrict__ seg_heads) {
-  extern __shared__ uint16_t hp4_head[];  // position - s + 1 (0 = none)
-  const WorkItem w = work[blockIdx.x];
-  const LaneDev L = lanes[w.lane];
-  const uint64_t n = L.n;
-  const uint64_t s = w.start;
-  const uint64_t e = umin64(s + HP4_SEG, n);
-  const int lane = threadIdx.x;
-  uint16_t* head = hp4_head;
-  uint4* h4 = reinterpret_cast<uint4*>(head);
-  for (int i = lane; i < 32768 * 2 / 16; i += 32) h4[i] = make_uint4(0, 0, 0, 0);
-  __syncwarp();
-  const uint8_t* src = L.src;
-  uint16_t* out = pd + L.pbase;
-  uint32_t wc, xc;
-  hp_load_tile(src, n, s, lane, wc, xc);
-  for (uint64_t c = s; c < e; c += 128) {
-    uint32_t wn = 0, xn = 0;
-    if (c + 128 < e) hp_load_tile(src, n, c + 128, lane, wn, xn);
-    // independent work of the 4 sub-steps first (hashes, same-hash groups) ...
-    uint32_t h[4];
-    unsigned peers[4];
-    bool valid[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint32_t i = 32 * k + lane;
-      const uint64_t q = c + i;
-      const uint32_t b0 = hp_byte(wc, xc, i), b1 = hp_byte(wc, xc, i + 1), b2 = hp_byte(wc, xc, i + 2);
-      valid[k] = q < e && q + MIN_MATCH <= n;
-      h[k] = valid[k] ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + lane;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; k++) peers[k] = __match_any_sync(0xffffffffu, h[k]);
-    // ... then the in-order head table traffic
-    uint32_t d[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint64_t q = c + 32 * k + lane;
-      const unsigned lower = peers[k] & ((1u << lane) - 1);
-      d[k] = 0;
-      if (valid[k]) {
-        if (lower) {
-          d[k] = lane - (31 - __clz(lower));
-        } else {
-          const uint32_t r = head[h[k]];
-          d[k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
-        }
-      }
-      __syncwarp();
-      if (valid[k] && (peers[k] >> lane) == 1u) head[h[k]] = (uint16_t)(q - s + 1);
-      __syncwarp();
-    }
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint64_t q = c + 32 * k + lane;
-      if (q < e) out[q] = (uint16_t)d[k];
-    }
-    wc = wn;
-    xc = xn;
-  }
-  __syncwarp();
-  uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)blockIdx.x * 32768);
-  for (int i = lane; i < 32768 * 2 / 16; i += 32) dst[i] = h4[i];
-}
-
-// K3 (block-parallel, current): one 1024-thread CTA per SM walks 32 Ki-position
-// segments 1024 positions (one chunk) at a time.  Within a warp,
-// __match_any_sync finds the previous lane with the same hash.  Across the 32
-// warps of a chunk, every same-hash group's leader (its last lane) sets its
-// warp's bit in a per-hash mask M[h] and enters (h, lane) in its warp's small
-// open-addressed table T.  A position without an earlier same-hash lane in its
-// warp takes the highest earlier warp in M[h] and looks its lane up in that
-// warp's T, or else reads the segment's head table H (last position of h in
-// earlier chunks).  The chunk's last group of each hash then updates H and
-// clears M[h]; leaders empty their T slots.  Three barriers per 1024 positions
-// instead of one in-order table update per 32; positions whose hash is new to the
-// segment get 0xffff and are resolved by k_hash_fix from the previous segment's
-// final table, as before.
-constexpr int HP5_THREADS = 1024;
-constexpr int HP5_TSLOTS = 64;  // per-warp (hash, lane) table
-constexpr size_t HP5_SMEM = 32768 * 4 + 32768 * 2 + (HP5_THREADS / 32) * HP5_TSLOTS * 4;
-
-__global__ void __launch_bounds__(HP5_THREADS, 1) k_hash_prev5(const LaneDev* __restrict__ lanes,
-                                                               const WorkItem* __restrict__ work, uint32_t nwork,
-                                                               uint16_t* __restrict__ pd,
-                                                               uint16_t* __restrict__ seg_heads) {
-  extern __shared__ __align__(16) uint8_t hp5_smem[];
-  uint32_t* M = reinterpret_cast<uint32_t*>(hp5_smem);              // 32768 warp masks
-  uint16_t* H = reinterpret_cast<uint16_t*>(hp5_smem + 32768 * 4);  // position - s + 1 (0 = none)
-  uint32_t* T = reinterpret_cast<uint32_t*>(hp5_smem + 32768 * 6);  // [warp][slot] = h << 8 | lane
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned below = (1u << lane) - 1;
-  {
-    uint4* m4 = reinterpret_cast<uint4*>(M);
-    for (int i = tid; i < 32768 * 4 / 16; i += HP5_THREADS) m4[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < (HP5_THREADS / 32) * HP5_TSLOTS; i += HP5_THREADS) T[i] = 0xffffffffu;
-  }
-  uint32_t* Tw = T + warp * HP5_TSLOTS;
-  for (uint32_t wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
-    const WorkItem w = work[wi];
-    const LaneDev L = lanes[w.lane];
-    const uint64_t n = L.n;
-    const uint64_t s = w.start;
-    const uint64_t e = umin64(s + HP4_SEG, n);
-    const uint8_t* src = L.src;
-    uint16_t* out = pd + L.pbase;
-    {
-      uint4* h4 = reinterpret_cast<uint4*>(H);
-      for (int i = tid; i < 32768 * 2 / 16; i += HP5_THREADS) h4[i] = make_uint4(0, 0, 0, 0);
-    }
-    // bytes of the first chunk (prefetched one chunk ahead from then on)
-    uint32_t b0 = 0, b1 = 0, b2 = 0;
-    {
-      const uint64_t q = s + tid;
-      if (q + MIN_MATCH <= n) b0 = __ldg(src + q), b1 = __ldg(src + q + 1), b2 = __ldg(src + q + 2);
-    }
-    __syncthreads();
-    for (uint64_t c = s; c < e; c += HP5_THREADS) {
-      const uint64_t q = c + tid;
-      const bool valid = q < e && q + MIN_MATCH <= n;
-      const uint32_t h = valid ? (((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff) : 0x10000u + tid;
-      {
-        const uint64_t qn = q + HP5_THREADS;
-        b0 = b1 = b2 = 0;
-        if (qn < e && qn + MIN_MATCH <= n) b0 = __ldg(src + qn), b1 = __ldg(src + qn + 1), b2 = __ldg(src + qn + 2);
-      }
-      const unsigned peers = __match_any_sync(0xffffffffu, h);
-      const bool leader = valid && (peers >> lane) == 1u;  // last lane of its group in this warp
-      uint32_t slot = 0;
-      if (leader) {
-        atomicOr(&M[h], 1u << warp);
-        slot = h & (HP5_TSLOTS - 1);
-        while (atomicCAS(&Tw[slot], 0xffffffffu, (h << 8) | lane) != 0xffffffffu) slot = (slot + 1) & (HP5_TSLOTS - 1);
-      }
-      __syncthreads();
-      uint32_t d = 0;
-      bool last = false;
-      if (valid) {
-        const unsigned lower = peers & below;
-        const uint32_t m = M[h];
-        last = leader && (m >> warp) == 1u;
-        if (lower) {
-          d = lane - (31 - __clz(lower));
-        } else {
-          const uint32_t mb = m & ((1u << warp) - 1);
-          if (mb) {
-            const int w2 = 31 - __clz(mb);
-            const uint32_t* T2 = T + w2 * HP5_TSLOTS;
-            uint32_t sl = h & (HP5_TSLOTS - 1), v;
-            while (((v = T2[sl]) >> 8) != h) sl = (sl + 1) & (HP5_TSLOTS - 1);
-            d = (uint32_t)(tid - (w2 * 32 + (int)(v & 31)));
-          } else {
-            const uint32_t r = H[h];
-            d = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;
-          }
-        }
-      }
-      __syncthreads();
-      if (leader) Tw[slot] = 0xffffffffu;
-      if (last) {
-        H[h] = (uint16_t)(q - s + 1);
-        M[h] = 0;
-      }
-      if (q < e) out[q] = (uint16_t)d;
-      __syncthreads();
-    }
-    uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)wi * 32768);
-    const uint4* h4 = reinterpret_cast<const uint4*>(H);
-    for (int i = tid; i < 32768 * 2 / 16; i += HP5_THREADS) dst[i] = h4[i];
-    __syncthreads();
-  }
-}
-
-// K3 (warp per segment, deep prefetch): k_hash_prev4's in-order scan with the
-// segment's bytes prefetched HP6_D tiles (HP6_D x 128 positions) ahead into
-// registers, so the warp's serial head-table chain is not also waiting on DRAM,
-// and the three hash bytes of a position taken from two shuffled words.
 constexpr int HP6_D = 8;
 
 __device__ __forceinline__ uint32_t hp_hash_at(uint32_t w, uint32_t x, int k, int lane) {
@@ -612,36 +307,6 @@ __global__ void __launch_bounds__(32) k_hash_prev6(const LaneDev* __restrict__ l
   for (int i = lane; i < 32768 * 2 / 16; i += 32) dst[i] = h4[i];
 }
 
-__global__ void k_hash_fix(const LaneDev* __restrict__ lanes, int nlanes, const uint64_t* __restrict__ lp,
-                           const uint32_t* __restrict__ seg0, uint64_t total, uint16_t* __restrict__ pd,
-                           const uint16_t* __restrict__ seg_heads) {
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = nlanes - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (lp[mid] <= g) lo = mid;
-      else hi = mid - 1;
-    }
-    const LaneDev& L = lanes[lo];
-    const uint64_t q = g - lp[lo];
-    uint16_t* slot = pd + L.pbase + q;
-    if (*slot != 0xffff) continue;
-    const uint64_t seg = q / HP4_SEG;
-    uint32_t d = 0;
-    if (seg > 0) {
-      const uint32_t h =
-          (((uint32_t)__ldg(L.src + q) << 10) ^ ((uint32_t)__ldg(L.src + q + 1) << 5) ^ __ldg(L.src + q + 2)) & 0x7fff;
-      const uint32_t r = seg_heads[(uint64_t)(seg0[lo] + seg - 1) * 32768 + h];
-      if (r) {
-        const uint64_t pred = (seg - 1) * HP4_SEG + r - 1;
-        const uint64_t dd = q - pred;
-        d = dd < WSIZE ? (uint32_t)dd : 0;
-      }
-    }
-    *slot = (uint16_t)d;
-  }
-}
-
 // k_hash_fix2: one CTA per segment, eight positions per thread and step
 // (one 16-byte load of their links); only positions marked 0xffff compute their
 // hash and read the previous segment's final head table.
@@ -714,130 +379,11 @@ static int hash_prev_two_phase(Workspace& sortws, Workspace& W, const LaneDev* d
   BB_CUDA_TRY(cudaMemcpyAsync(d_work, work.data(), sizeof(WorkItem) * work.size(), cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_seg0, seg0.data(), 4 * nl, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
-  static const int k3_variant = getenv("BB_K3_VARIANT") ? atoi(getenv("BB_K3_VARIANT")) : 6;
-  if (k3_variant == 4) {
-    k_hash_prev4<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
-  } else if (k3_variant == 6) {
-    k_hash_prev6<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
-  } else {
-    const unsigned grid = (unsigned)std::min<size_t>(work.size(), kNumSMs);
-    k_hash_prev5<<<grid, HP5_THREADS, HP5_SMEM, st>>>(d_lanes, d_work, (uint32_t)work.size(), d_pd, heads);
-  }
+  k_hash_prev6<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
   BB_LAUNCH_CHECK();
   k_hash_fix2<<<(unsigned)work.size(), 256, 0, st>>>(d_lanes, d_work, d_pd, heads);
   BB_LAUNCH_CHECK();
   return BB_OK;
-}
-
-// K3 (device-wide sort): every position of every lane gets the key
-// (lane << 16 | hash) -- or (lane << 16 | 0x8000) when fewer than 3 bytes
-// remain -- and one stable LSD radix sort (CUB onesweep) brings equal hashes of
-// a lane together in position order; the previous element of a run is the
-// previous same-hash position.  O(n) work, bandwidth-bound.
-__global__ void k_hash_keys(const LaneDev* __restrict__ lanes, int nlanes, const uint64_t* __restrict__ lp,
-                            uint64_t total, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = nlanes - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (lp[mid] <= g) lo = mid;
-      else hi = mid - 1;
-    }
-    const LaneDev& L = lanes[lo];
-    const uint64_t q = g - lp[lo];
-    uint32_t k = 0x8000;
-    if (q + MIN_MATCH <= L.n)
-      k = (((uint32_t)__ldg(L.src + q) << 10) ^ ((uint32_t)__ldg(L.src + q + 1) << 5) ^ __ldg(L.src + q + 2)) & 0x7fff;
-    keys[g] = ((uint32_t)lo << 16) | k;
-    vals[g] = (uint32_t)q;
-  }
-}
-
-__global__ void k_links(const LaneDev* __restrict__ lanes, uint64_t total, const uint32_t* __restrict__ keys,
-                        const uint32_t* __restrict__ vals, uint16_t* __restrict__ pd) {
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys[g], q = vals[g];
-    uint32_t d = 0;
-    if (!(k & 0x8000) && g > 0 && keys[g - 1] == k) {
-      const uint32_t dd = q - vals[g - 1];
-      d = dd < WSIZE ? dd : 0;
-    }
-    pd[lanes[k >> 16].pbase + q] = (uint16_t)d;
-  }
-}
-
-// K3 (sort-based): one CTA of 1024 threads per HP2_SEG positions with a
-// 32768-entry u32 head table in shared memory.  The 32 KiB history only needs
-// each hash's most recent position, so it is inserted order-free with
-// atomicMax.  Segment positions go 1024 at a time through a stable block radix
-// sort on the 15-bit hash: equal hashes become adjacent in position order, so a
-// position's predecessor is its sorted neighbour (or the head table), and the
-// last of each run updates the head.
-constexpr uint32_t HP2_SEG = 32768;
-constexpr int HP2_THREADS = 1024;
-
-__global__ void __launch_bounds__(HP2_THREADS, 1) k_hash_prev2(const LaneDev* __restrict__ lanes,
-                                                               const WorkItem* __restrict__ work,
-                                                               uint16_t* __restrict__ pd) {
-  typedef cub::BlockRadixSort<uint16_t, HP2_THREADS, 1, uint16_t> Sort;
-  extern __shared__ __align__(16) uint32_t hp2_smem[];
-  uint32_t* head = hp2_smem;  // 32768: position + 1 (0 = none)
-  __shared__ typename Sort::TempStorage sort_tmp;
-  __shared__ uint16_t s_key[HP2_THREADS];
-  __shared__ uint16_t s_val[HP2_THREADS];
-  __shared__ uint16_t s_out[HP2_THREADS];
-  const WorkItem w = work[blockIdx.x];
-  const LaneDev L = lanes[w.lane];
-  const uint64_t n = L.n;
-  const uint64_t s = w.start;
-  const uint64_t e = umin64(s + HP2_SEG, n);
-  const uint64_t base = s > WSIZE ? s - WSIZE : 0;
-  const uint8_t* src = L.src;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < 32768; i += HP2_THREADS) head[i] = 0;
-  __syncthreads();
-  // history: most recent position per hash, scanned from the newest end so a
-  // hash already set by a later position needs no atomic (low-entropy lanes
-  // would otherwise serialise on a few hot buckets)
-  for (uint64_t off = tid; off < s - base; off += HP2_THREADS) {
-    const uint64_t q = s - 1 - off;
-    if (q + MIN_MATCH > n) continue;
-    uint32_t h = (((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^ __ldg(src + q + 2)) & 0x7fff;
-    if (head[h] < (uint32_t)(q - base + 1)) atomicMax(&head[h], (uint32_t)(q - base + 1));
-  }
-  __syncthreads();
-  uint16_t* out = pd + L.pbase;
-  for (uint64_t c = s; c < e; c += HP2_THREADS) {
-    const uint64_t q = c + tid;
-    const bool valid = q < e && q + MIN_MATCH <= n;
-    uint16_t key[1], val[1];
-    key[0] = valid ? (uint16_t)((((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^
-                                 __ldg(src + q + 2)) & 0x7fff)
-                   : (uint16_t)0xffff;
-    val[0] = (uint16_t)tid;
-    Sort(sort_tmp).Sort(key, val, 0, 16);
-    // sorted order: thread i holds rank i
-    s_key[tid] = key[0];
-    s_val[tid] = val[0];
-    __syncthreads();
-    const uint16_t k = key[0], v = val[0];
-    uint32_t d = 0;
-    if (k != 0xffff) {
-      const uint64_t qq = c + v;
-      uint64_t pred = ~0ull;
-      if (tid > 0 && s_key[tid - 1] == k) {
-        pred = c + s_val[tid - 1];
-      } else if (head[k]) {
-        pred = base + head[k] - 1;
-      }
-      if (pred != ~0ull && qq - pred < WSIZE) d = (uint32_t)(qq - pred);
-    }
-    s_out[v] = (uint16_t)d;
-    __syncthreads();
-    if (k != 0xffff && (tid == HP2_THREADS - 1 || s_key[tid + 1] != k)) head[k] = (uint32_t)(c + v - base + 1);
-    if (q < e) out[q] = s_out[tid];
-    __syncthreads();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -856,222 +402,6 @@ __device__ __forceinline__ uint32_t prof_pack(uint32_t best, uint32_t bestd) {
 // + bytes 0,1) and the word at candidate + best_len - 1 (bytes best-1, best --
 // zlib's scan_end1 / scan_end quick reject).
 constexpr uint32_t PF_WIN = WSIZE + PF_SEG + MAX_MATCH + 32;
-
-__global__ void __launch_bounds__(PF_THREADS, 1) k_profile(const LaneDev* __restrict__ lanes,
-                                                           const WorkItem* __restrict__ work,
-                                                           const uint16_t* __restrict__ pd,
-                                                           uint2* __restrict__ prof) {
-  extern __shared__ __align__(16) uint32_t w32[];
-  const WorkItem w = work[blockIdx.x];
-  const LaneDev L = lanes[w.lane];
-  const uint64_t n = L.n;
-  const uint64_t s = w.start;
-  const uint64_t e = umin64(s + PF_SEG, n);
-  const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
-  const uint32_t wlen = (uint32_t)(e - wlo) + MAX_MATCH + 16;  // <= PF_WIN
-  const uint8_t* src = L.src;
-  const uint16_t* pdl = pd + L.pbase;
-  for (uint32_t i = threadIdx.x; i < wlen; i += blockDim.x) {
-    const uint64_t q = wlo + i;
-    uint32_t v = 0xffff;
-    if (q < e) {
-      const uint32_t l = pdl[q];
-      v = l ? l : 0xffff;
-    }
-    if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
-    if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
-    w32[i] = v;
-  }
-  __syncthreads();
-
-  for (uint64_t p = s + threadIdx.x; p < e; p += blockDim.x) {
-    const uint32_t ip = (uint32_t)(p - wlo);
-    const uint32_t wp = w32[ip];
-    const uint32_t d0 = wp & 0xffff;  // 0xffff = no earlier position with this hash
-    uint2 res = make_uint2(0, 0);
-    if (p + MIN_MATCH <= n && d0 <= MAX_DIST && p != d0) {
-      const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
-      const uint32_t nice = min(NICE_LENGTH, la);
-      const uint32_t maxl = min(MAX_MATCH, la);
-      const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
-      // candidates continue while (window index) > lim_s; -1 when the limit lies before the window
-      const int lim_s = limit >= wlo ? (int)(limit - wlo) : -1;
-      const uint32_t flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
-      const uint32_t s01 = wp & 0xffff0000u;
-      uint32_t best = MIN_MATCH - 1, bestd = 0, r32 = 0;
-      uint32_t se01 = w32[ip + best - 1] & 0xffff0000u;
-      int ic = (int)(ip - d0);
-      int cnt = 0;
-      bool stop = false;
-      // one chain step: quick reject on bytes (0,1) and (best-1,best), then extend
-#define PF_STEP()                                                                 \
-  {                                                                               \
-    const uint32_t wc = w32[ic];                                                  \
-    const uint32_t we = w32[ic + best - 1];                                       \
-    if ((((wc & 0xffff0000u) ^ s01) | ((we & 0xffff0000u) ^ se01)) == 0) {       \
-      uint32_t len = 2;                                                           \
-      while (len < maxl) {                                                        \
-        const uint32_t x = (w32[ic + len] ^ w32[ip + len]) >> 16;                 \
-        if (x) {                                                                  \
-          len += (x & 0xff) == 0;                                                 \
-          break;                                                                  \
-        }                                                                         \
-        len += 2;                                                                 \
-      }                                                                           \
-      len = min(len, maxl);                                                       \
-      if (len > best) {                                                           \
-        best = len;                                                               \
-        bestd = ip - (uint32_t)ic;                                                \
-        if (len >= nice) {                                                        \
-          stop = true;                                                            \
-          break;                                                                  \
-        }                                                                         \
-        se01 = w32[ip + best - 1] & 0xffff0000u;                                  \
-      }                                                                           \
-    }                                                                             \
-    const int nx = ic - (int)(wc & 0xffff);                                       \
-    if (nx <= lim_s) {                                                            \
-      stop = true;                                                                \
-      break;                                                                      \
-    }                                                                             \
-    ic = nx;                                                                      \
-  }
-      for (cnt = 1; cnt <= 32; cnt++) PF_STEP();
-      r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
-      if (!stop)
-        for (cnt = 33; cnt <= (int)MAX_CHAIN; cnt++) PF_STEP();
-#undef PF_STEP
-      res.x = prof_pack(best, bestd) | flag;
-      res.y = r32 | flag;
-    }
-    prof[L.pbase + p] = res;
-  }
-}
-
-// K4 (current): the same first-maximum search with two changes that remove most
-// of the warp divergence of the chain walk:
-//  * window word = (1-based window index of the previous same-hash position,
-//    0 = none) | bytes (q, q+1) << 16, so a chain step is: load the candidate's
-//    word, load bytes (best-1, best) of the candidate, one byte_perm compare,
-//    and the next link is the low half -- the limit test "index > lim1" also
-//    catches "none";
-//  * a candidate passing the quick reject is not extended at once (which ran
-//    the extension loop for one lane while 31 waited).  It is parked in the
-//    lane's pending slot and extended later, together with the pending
-//    candidates of the other lanes: when some lane passes again while it still
-//    has one parked, at the budget-32 snapshot and at the end.  best only
-//    changes in those flushes, so a parked candidate is judged against exactly
-//    the best it was tested with, and a candidate tested while another was
-//    parked that fails the quick reject cannot beat the flushed best either (it
-//    mismatches at or before the old best).  Exact first-maximum semantics.
-__global__ void __launch_bounds__(PF_THREADS, 1) k_profile2(const LaneDev* __restrict__ lanes,
-                                                            const WorkItem* __restrict__ work,
-                                                            const uint16_t* __restrict__ pd,
-                                                            uint2* __restrict__ prof) {
-  extern __shared__ __align__(16) uint32_t w32[];
-  const WorkItem w = work[blockIdx.x];
-  const LaneDev L = lanes[w.lane];
-  const uint64_t n = L.n;
-  const uint64_t s = w.start;
-  const uint64_t e = umin64(s + PF_SEG, n);
-  const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
-  const uint32_t wlen = (uint32_t)(e - wlo) + MAX_MATCH + 16;  // <= PF_WIN
-  const uint8_t* src = L.src;
-  const uint16_t* pdl = pd + L.pbase;
-  for (uint32_t i = threadIdx.x; i < wlen; i += blockDim.x) {
-    const uint64_t q = wlo + i;
-    uint32_t v = 0;
-    if (q < e) {
-      const uint32_t l = pdl[q];
-      if (l && l <= i) v = i - l + 1;  // predecessor inside the window
-    }
-    if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
-    if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
-    w32[i] = v;
-  }
-  __syncthreads();
-  const char* wb = reinterpret_cast<const char*>(w32);
-
-  for (uint64_t p0 = s; p0 < e; p0 += blockDim.x) {
-    const uint64_t p = p0 + threadIdx.x;
-    uint2 res = make_uint2(0, 0);
-    const uint32_t ip = (uint32_t)(p - wlo);
-    const uint32_t wp = p < e ? w32[ip] : 0;
-    const uint32_t c0 = wp & 0xffff;  // 1-based index of the first candidate
-    const uint32_t d0 = ip + 1 - c0;
-    bool alive = p < e && p + MIN_MATCH <= n && c0 != 0 && d0 <= MAX_DIST && wlo + c0 - 1 != 0;
-    // the warp walks while any lane is alive (uniform control flow)
-    uint32_t best = MIN_MATCH - 1, bestd = 0, r32 = 0, flag = 0;
-    uint32_t la = 0, nice = 0, maxl = 0, lim1 = 0, key = 0, off = 0, ic1 = 1, q0 = 0;
-    bool has = false;
-    if (alive) {
-      la = (uint32_t)umin64(n - p, 1u << 20);
-      nice = min(NICE_LENGTH, la);
-      maxl = min(MAX_MATCH, la);
-      const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
-      lim1 = limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0;
-      flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
-      key = (wp >> 16) | (w32[ip + best - 1] & 0xffff0000u);
-      off = 4 * (best - 1) + 2;  // byte offset from word (ic1 - 1) to the high half of word (ic1 + best - 2)
-      ic1 = c0;
-    }
-    // extend the parked candidate (lanes with one), judge it against best
-    auto flush = [&]() {
-      if (has) {
-        const uint32_t ic = q0 - 1;
-        uint32_t len = 2;
-        while (len < maxl) {
-          const uint32_t x = (w32[ic + len] ^ w32[ip + len]) >> 16;
-          if (x) {
-            len += (x & 0xff) == 0;
-            break;
-          }
-          len += 2;
-        }
-        len = min(len, maxl);
-        if (len > best) {
-          best = len;
-          bestd = ip - ic;
-          if (len >= nice) alive = false;
-          key = (wp >> 16) | (w32[ip + best - 1] & 0xffff0000u);
-          off = 4 * (best - 1) + 2;
-        }
-        has = false;
-      }
-    };
-    auto step = [&]() {
-      const uint32_t wc = *reinterpret_cast<const uint32_t*>(wb + 4 * (ic1 - 1));
-      uint32_t we = *reinterpret_cast<const uint16_t*>(wb + 4 * (ic1 - 1) + off);
-      bool pass = alive && __byte_perm(wc, we, 0x5432) == key;
-      if (__any_sync(0xffffffffu, pass && has)) {
-        flush();
-        we = *reinterpret_cast<const uint16_t*>(wb + 4 * (ic1 - 1) + off);
-        pass = alive && __byte_perm(wc, we, 0x5432) == key;
-      }
-      if (pass) {
-        q0 = ic1;
-        has = true;
-      }
-      const uint32_t nx = wc & 0xffff;
-      alive = alive && nx > lim1;
-      if (alive) ic1 = nx;
-    };
-    for (int cnt = 0; cnt < 32; cnt += 4) {
-      if (!__any_sync(0xffffffffu, alive)) break;
-      step(); step(); step(); step();
-    }
-    flush();
-    r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
-    for (int cnt = 32; cnt < (int)MAX_CHAIN; cnt += 4) {
-      if (!__any_sync(0xffffffffu, alive)) break;
-      step(); step(); step(); step();
-    }
-    flush();
-    res.x = prof_pack(best, bestd) | flag;
-    res.y = r32 | flag;
-    if (p < e) prof[L.pbase + p] = res;
-  }
-}
 
 // K4 (current): first-maximum chain search with the passes of each lane
 // batched.  Window word (shared memory, word 0 = a dead-end sentinel):
@@ -2246,46 +1576,12 @@ __global__ void k_container_header(const ContainerDev* __restrict__ cons, int nc
 
 
 // K3 launcher (key generation, CUB onesweep radix sort, link scatter)
-static int hash_prev_sorted(Workspace& sortws, Workspace& W, const LaneDev* d_lanes, int nl,
-                            const std::vector<uint64_t>& lane_prefix, uint16_t* d_pd, cudaStream_t st,
-                            StageTimer* T = nullptr) {
-  const uint64_t npos_exact = lane_prefix[nl];
-  int lane_bits = 1;
-  while ((1 << lane_bits) < nl) lane_bits++;
-  if (nl > 65535 || npos_exact >= (1ull << 31)) {
-    set_error("deflate: too many lanes/positions in one call");
-    return BB_ERROR;
-  }
-  size_t tmp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)npos_exact, 0, 16 + lane_bits, st);
-  int rc = sortws.reserve(16 * npos_exact + tmp_bytes + 4096);
-  if (rc) return rc;
-  uint32_t* k0 = sortws.take<uint32_t>(npos_exact);
-  uint32_t* k1 = sortws.take<uint32_t>(npos_exact);
-  uint32_t* v0 = sortws.take<uint32_t>(npos_exact);
-  uint32_t* v1 = sortws.take<uint32_t>(npos_exact);
-  void* tmp = sortws.take<uint8_t>(tmp_bytes);
-  uint64_t* d_lp = W.take<uint64_t>(nl + 1);
-  BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
-  if (T) T->mark("deflate.k3_keys");
-  k_hash_keys<<<grid_for(npos_exact, 256, 16), 256, 0, st>>>(d_lanes, nl, d_lp, npos_exact, k0, v0);
-  BB_LAUNCH_CHECK();
-  if (T) T->mark("deflate.k3_sort");
-  BB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int)npos_exact, 0, 16 + lane_bits, st));
-  count_launch(4);
-  if (T) T->mark("deflate.k3_links");
-  k_links<<<grid_for(npos_exact, 256, 16), 256, 0, st>>>(d_lanes, npos_exact, k1, v1, d_pd);
-  BB_LAUNCH_CHECK();
-  return BB_OK;
-}
-
 // ---------------------------------------------------------------------------
 // host orchestration
 
 struct DeflateEngine {
   Workspace ws;
-  Workspace sortws;  // keys/values (x2) + CUB temp storage for K3
+  Workspace sortws;  // K3's per-segment final head tables
   bool tables_ready = false;
   uint64_t* h_pinned = nullptr;  // small pinned scratch for results
   size_t h_pinned_cap = 0;
@@ -2315,13 +1611,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   if (!e->tables_ready) {
     ZTables t = make_tables();
     BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev4, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HP5_SMEM));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile2, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
     e->tables_ready = true;
   }
@@ -2452,25 +1742,13 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
 
   // K3, K4
   T.mark("deflate.hash_prev");
-  static const int k3_sorted = getenv("BB_K3_SORT") ? 1 : 0;
-  if (npos_exact && k3_sorted) {
-    rc = hash_prev_sorted(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st, &T);
-    if (rc) return rc;
-  } else if (npos_exact) {
+  if (npos_exact) {
     rc = hash_prev_two_phase(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
     if (rc) return rc;
   }
   T.mark("deflate.profile");
   if (!pf_work.empty()) {
-    size_t smem = 4 * PF_WIN;
-    static const int k4_old = getenv("BB_K4_OLD") ? 1 : 0;
-    static const int k4_var = getenv("BB_K4_VARIANT") ? atoi(getenv("BB_K4_VARIANT")) : 3;
-    if (k4_old || k4_var == 1)
-      k_profile<<<(unsigned)pf_work.size(), PF_THREADS, smem, st>>>(d_lanes, d_pf, d_pd, d_prof);
-    else if (k4_var == 2)
-      k_profile2<<<(unsigned)pf_work.size(), PF_THREADS, smem, st>>>(d_lanes, d_pf, d_pd, d_prof);
-    else
-      k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, smem + 16, st>>>(d_lanes, d_pf, d_pd, d_prof);
+    k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof);
     BB_LAUNCH_CHECK();
   }
   // K5: speculative parse, then fix-up rounds until no exit state changes
@@ -2571,11 +1849,8 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ZTables t = make_tables();
   BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
-  BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev2, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev3, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-  BB_CUDA_TRY(cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile2, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
   LaneDev d{};
   d.src = d_in;
   d.n = n;
@@ -2590,18 +1865,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   BB_CUDA_TRY(cudaMemcpy(dl, &d, sizeof d, cudaMemcpyHostToDevice));
   if (!hp.empty()) BB_CUDA_TRY(cudaMemcpy(dh, hp.data(), sizeof(WorkItem) * hp.size(), cudaMemcpyHostToDevice));
   if (!pf.empty()) BB_CUDA_TRY(cudaMemcpy(dp, pf.data(), sizeof(WorkItem) * pf.size(), cudaMemcpyHostToDevice));
-  if (n && getenv("BB_K3_SORT")) {
-    Workspace sw, w2;
-    int rc = w2.reserve(4096);
-    if (rc) return rc;
-    std::vector<uint64_t> lp{0, n};
-    rc = hash_prev_sorted(sw, w2, dl, 1, lp, d_pd, st);
-    if (rc) return rc;
-    BB_CUDA_TRY(cudaStreamSynchronize(st));
-  } else if (n) {
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev4, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HP5_SMEM));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  if (n) {
     Workspace sw, w2;
     int rc = w2.reserve(4096 + 16 * (n / HP4_SEG + 2));
     if (rc) return rc;

@@ -7,25 +7,28 @@
 // known after Huffman-decoding their predecessors.  Instead of walking them in
 // order, every place a block could start is found and decoded at once:
 //
-//   P1 k_candidates   every bit offset is tested for a dynamic-block header
-//                     (BTYPE=10, HLIT<=29, HDIST<=29, complete code-length code);
-//                     every byte offset for a stored block (LEN == ~NLEN);
-//                     results are bitmaps, so ranks give ordered node ids
-//   P2 k_decode_nodes one thread per candidate: full header validation + symbol
-//                     decode to end-of-block (plus any static blocks that follow),
-//                     recording end bit, output bytes and match count
+//   P1 k_candidates4  every bit offset is tested for a dynamic-block header
+//                     (BTYPE=10, HLIT<=29, HDIST<=29 bit-sliced over 32 offsets,
+//                     then a complete code-length code), survivors verified
+//                     exactly by k_verify_dynamic; every byte offset for a stored
+//                     block (LEN == ~NLEN); bitmaps, so ranks give ordered node ids
+//   P2 k_decode_nodes stored / static candidates: one thread each;
+//      k_dyn_scan     dynamic candidates: one warp each, the block's bits cut into
+//                     32 chunks decoded at once (Huffman self-synchronisation,
+//                     Jacobi fix-up), recording end bit, output bytes, matches
 //   P3 k_link         each node's successor = the candidate that starts exactly
 //                     where it ends (or END / BREAK / BAD)
 //   P4 binary lifting the true block chain is the path from the zlib header;
 //                     jump tables give the i-th block of the chain in O(log)
-//   P5 k_emit_nodes   second decode of the chain's blocks at their final output
-//                     offsets: literals written, matches recorded as (dst,dist,len);
-//                     stored blocks copied by whole CTAs; a BREAK (static block)
-//                     is finished by one thread (k_tail)
-//   P6 LZ77 resolution per 32 KiB output window: pointer jumping in shared
-//                     memory resolves every match byte whose source chain stays in
-//                     the window; the rest are resolved window by window in order
-//                     (k_resolve_ext: one gather per window)
+//   P5 k_dyn_emit     second decode of the chain's dynamic blocks at their final
+//                     output offsets: literals written, matches recorded as
+//                     (dst,dist,len); k_copy_stored copies stored blocks; a BREAK
+//                     (static block) is finished by one thread (k_tail)
+//   P6 LZ77 resolution: pointer jumping in shared memory over 32 KiB windows
+//                     (k_resolve_local) or 2-window thread-block clusters
+//                     (k_resolve_cluster, distributed shared memory); bytes whose
+//                     copy chain leaves the window chase a read-only source map
+//                     to a resolved byte (k_resolve_chase)
 //   P7 Adler-32 check, size check
 #include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
@@ -429,51 +432,6 @@ __device__ __forceinline__ bool dyn_header_quick(uint64_t w0, uint64_t w1, uint3
 // Survivors of the quick test are appended to a list (warp-aggregated) and
 // verified exactly by k_verify_dynamic with one thread each, so the rare long
 // verifications do not serialise whole warps.
-__global__ void k_candidates(const PJob* __restrict__ jobs, const uint64_t* __restrict__ blk_prefix, int njobs,
-                             uint32_t* __restrict__ dbm,
-                             uint32_t* __restrict__ sbm, int find_dynamic, uint64_t* __restrict__ surv,
-                             unsigned long long* __restrict__ surv_cnt, uint64_t surv_cap) {
-  const uint32_t j = (uint32_t)find_job(blk_prefix, njobs, blockIdx.x);
-  const PJob J = jobs[j];
-  const uint64_t B = (blockIdx.x - blk_prefix[j]) * 256ull + threadIdx.x;  // one stream byte per thread
-  const int lane = threadIdx.x & 31;
-  uint32_t dbits = 0;
-  bool st = false;
-  if (B < J.n) {
-    if (find_dynamic) {
-      const uint64_t w0 = peek64(J.src, J.n, 8 * B), w1 = peek64(J.src, J.n, 8 * B + 64);
-      for (uint32_t k = 0; k < 8; k++) {
-        const uint64_t b = 8 * B + k;
-        if (b >= 16 && b + 17 <= 8 * J.n && dyn_header_quick(w0, w1, k)) dbits |= 1u << k;
-      }
-    }
-    if (B >= 2 && B + 4 <= J.n) {
-      uint32_t len = __ldg(J.src + B) | ((uint32_t)__ldg(J.src + B + 1) << 8);
-      uint32_t nlen = __ldg(J.src + B + 2) | ((uint32_t)__ldg(J.src + B + 3) << 8);
-      st = len == (~nlen & 0xffff) && B + 4 + len <= J.n;
-    }
-  }
-  // survivors: one atomic per warp (warp-aggregated append)
-  {
-    const uint32_t cnt = __popc(dbits);
-    uint32_t pre = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += v;
-    }
-    const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
-    unsigned long long base = 0;
-    if (lane == 0 && tot) base = atomicAdd(surv_cnt, (unsigned long long)tot);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    uint64_t slot = base + pre - cnt;
-    for (uint32_t v = dbits; v; v &= v - 1, slot++)
-      if (slot < surv_cap) surv[slot] = ((uint64_t)j << 48) | (8 * B + (__ffs(v) - 1));
-  }
-  unsigned ball = __ballot_sync(0xffffffffu, st);
-  if (lane == 0 && B < J.n + 32) sbm[J.sbm + (B >> 5)] = ball;
-}
-
-
 // P1 (current): four stream bytes / 32 bit offsets per thread.  The cheap
 // header conditions (BTYPE = 10, HLIT <= 29, HDIST <= 29) are evaluated for all
 // 32 offsets at once on a 64-bit window (bit-sliced), and only the ~20 % that
@@ -755,52 +713,6 @@ __device__ __forceinline__ void fast_build(const Tables* T, FastT* F, int lane) 
   __syncwarp();
 }
 
-// dsym with the direct tables (same results and errors as dsym)
-__device__ __forceinline__ int dsymf(BitReader& r, const Tables* T, const FastT* F, const Lims& LL, const Lims& DL,
-                                     uint32_t& len, uint32_t& dist, uint32_t& lit) {
-  r.refill();
-  const uint32_t e = F->lit[(uint32_t)r.hold & ((1u << FAST_BITS) - 1)];
-  if (e & 15) {
-    r.drop(e & 15);
-    if (r.past_end()) return -1;
-    const uint32_t kind = (e >> 4) & 3;
-    if (kind == 0) {
-      lit = e >> 16;
-      len = 1;
-      return 0;
-    }
-    if (kind == 2) return 2;
-    if (kind == 3) return -1;
-    len = (e >> 16) + r.take((e >> 6) & 15);
-  } else {
-    int sym = hdecode(r, &T->lit);  // long code: limits from shared memory
-    if (sym < 0) return -1;
-    if (sym < 256) {
-      lit = (uint32_t)sym;
-      len = 1;
-      return 0;
-    }
-    if (sym == 256) return 2;
-    sym -= 257;
-    if (sym >= 29) return -1;
-    len = p_lbase[sym] + r.take(p_lext[sym]);
-  }
-  r.refill();
-  const uint32_t ed = F->dist[(uint32_t)r.hold & ((1u << FAST_DBITS) - 1)];
-  if (ed & 15) {
-    r.drop(ed & 15);
-    if (r.past_end()) return -1;
-    if (((ed >> 4) & 3) == 3) return -1;
-    dist = (ed >> 16) + r.take((ed >> 6) & 15);
-  } else {
-    int ds = hdecode(r, &T->dist);
-    if (ds < 0 || ds >= 30) return -1;
-    dist = p_dbase[ds] + r.take(p_dext[ds]);
-  }
-  if (r.past_end()) return -1;
-  return 1;
-}
-
 // Word-refill bit reader for the hot decode loops: a 64-bit window refilled
 // 32 bits at a time from aligned words (one 32-bit load per refill instead of
 // peek64's unaligned pair), positions counted as 32-bit offsets from the range
@@ -907,27 +819,6 @@ struct WarpSm {
   uint16_t rout[32][REC];  // output bytes before record j of the lane (<= REC * 258)
   uint16_t rnm[32][REC];   // matches before record j
 };
-
-// one lit/len symbol (+ distance): 0 literal, 1 match, 2 end of block, -1 invalid
-__device__ __forceinline__ int dsym(BitReader& r, const Tables* T, const Lims& LL, const Lims& DL, uint32_t& len,
-                                    uint32_t& dist, uint32_t& lit) {
-  int sym = hdecode(r, &T->lit, LL);
-  if (sym < 0) return -1;
-  if (sym < 256) {
-    lit = (uint32_t)sym;
-    len = 1;
-    return 0;
-  }
-  if (sym == 256) return 2;
-  sym -= 257;
-  if (sym >= 29) return -1;
-  len = p_lbase[sym] + r.take(p_lext[sym]);
-  int ds = hdecode(r, &T->dist, DL);
-  if (ds < 0 || ds >= 30) return -1;
-  dist = p_dbase[ds] + r.take(p_dext[ds]);
-  if (r.past_end()) return -1;
-  return 1;
-}
 
 __global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __restrict__ jobs,
                                                            const uint32_t* __restrict__ node_job,
@@ -1411,49 +1302,6 @@ __global__ void __launch_bounds__(256) k_chain_scan(const PJob* __restrict__ job
   }
 }
 
-// ---- P5 --------------------------------------------------------------------
-__global__ void __launch_bounds__(ND_THREADS) k_emit_nodes(const PJob* __restrict__ jobs, int njobs,
-                                                           const Chain* __restrict__ chains,
-                                                           const uint32_t* __restrict__ chain_nodes,
-                                                           const uint32_t* __restrict__ job_of_chain_block,
-                                                           const uint32_t* __restrict__ chain_block_base,
-                                                           const Node* __restrict__ nodes,
-                                                           const uint64_t* __restrict__ out_off,
-                                                           const uint64_t* __restrict__ m_off, Match* __restrict__ matches,
-                                                           uint32_t* __restrict__ fail) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  Tables* T = reinterpret_cast<Tables*>(sm) + threadIdx.x;
-  const uint32_t j = job_of_chain_block[blockIdx.x];
-  const PJob J = jobs[j];
-  const uint32_t i = (blockIdx.x - chain_block_base[j]) * blockDim.x + threadIdx.x;
-  if (i >= chains[j].len) return;
-  const Node nd = nodes[chain_nodes[J.node0 + i]];
-  if (nd.flags & 4) return;  // stored: copied by k_copy_stored
-  if (!(nd.flags & 8)) return;  // dynamic: k_dyn_emit (one warp per block)
-  const uint64_t off = out_off[J.node0 + i];
-  Match* mm = matches + J.mbase + m_off[J.node0 + i];
-  BitReader r;
-  r.init(J.src, J.n, nd.start);
-  uint32_t hdr = r.take(3);
-  bool final_seen = hdr & 1;
-  uint64_t out_len = 0;
-  uint32_t nmatch = 0;
-  const uint64_t limit = nd.out_len;
-  int rc = read_dynamic(r, T);
-  if (!rc) rc = decode_codes<true>(r, T, out_len, nmatch, limit, J.dst, off, mm, nd.nmatch);
-  while (!rc && !final_seen) {
-    r.refill();
-    uint32_t h = r.peek(3);
-    if (((h >> 1) & 3) != 1) break;
-    r.drop(3);
-    static_tables(T);
-    rc = decode_codes<true>(r, T, out_len, nmatch, limit, J.dst, off, mm, nd.nmatch);
-    final_seen = h & 1;
-  }
-  if (rc || out_len != nd.out_len) atomicExch(&fail[j], 1u);
-}
-
-// stored blocks of the chain: one CTA per block, byte-parallel copy
 __global__ void k_copy_stored(const PJob* __restrict__ jobs, const Chain* __restrict__ chains,
                               const uint32_t* __restrict__ chain_nodes, const Node* __restrict__ nodes,
                               const uint64_t* __restrict__ out_off, const uint32_t* __restrict__ job_of_block,
@@ -1940,7 +1788,6 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   size_t nd_smem = sizeof(Tables) * ND_THREADS;
   if (!attr) {
     BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_emit_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
