@@ -787,43 +787,46 @@ struct TreeArr {
   uint16_t freq[ELEMS];
   uint16_t code[ELEMS];
   uint16_t dad[2 * ELEMS + 1];
-  uint16_t len[2 * ELEMS + 2];  // +1: scan_tree guard slot
+  uint8_t len[2 * ELEMS + 2];  // +1: scan_tree guard slot (code lengths <= 15)
 };
 
 struct TreesState {
   TreeArr<L_CODES> lt;
   TreeArr<D_CODES> dt;
   TreeArr<BL_CODES> blt;
-  alignas(16) uint64_t heap[HEAP_SIZE + 1];
+  alignas(16) uint32_t heap[HEAP_SIZE + 1];
   uint16_t bl_count[16];
   uint64_t opt_len, static_len;
   int lmax, dmax, blmax;
 };
 
-__device__ __forceinline__ uint64_t t_entry(uint32_t freq, uint32_t depth, uint32_t node) {
-  return ((uint64_t)freq << 32) | (depth << 16) | node;
+// Heap entries pack (freq, depth, node) so one compare orders them as trees.c's
+// smaller(): freq (15 bits: a block has <= 16384 symbols + 2 forced nodes) |
+// depth (5 bits: a tree over <= 16386 counts is at most 21 deep) | node (10 bits).
+__device__ __forceinline__ uint32_t t_entry(uint32_t freq, uint32_t depth, uint32_t node) {
+  return (freq << 15) | (depth << 10) | node;
 }
-__device__ __forceinline__ uint32_t t_node(uint64_t e) { return (uint32_t)(e & 0xffff); }
-__device__ __forceinline__ uint32_t t_freq(uint64_t e) { return (uint32_t)(e >> 32); }
-__device__ __forceinline__ uint32_t t_depth(uint64_t e) { return (uint32_t)((e >> 16) & 0xffff); }
+__device__ __forceinline__ uint32_t t_node(uint32_t e) { return e & 0x3ff; }
+__device__ __forceinline__ uint32_t t_freq(uint32_t e) { return e >> 15; }
+__device__ __forceinline__ uint32_t t_depth(uint32_t e) { return (e >> 10) & 0x1f; }
 
 // trees.c pqdownheap with smaller(n, m) == key(n) <= key(m)
-__device__ __forceinline__ void t_down(uint64_t* heap, int heap_len, int k) {
-  const uint64_t v = heap[k];
-  const uint64_t vk = v >> 16;
+__device__ __forceinline__ void t_down(uint32_t* heap, int heap_len, int k) {
+  const uint32_t v = heap[k];
+  const uint32_t vk = v >> 10;
   int j = k << 1;
   while (j <= heap_len) {
-    // j is even: both sons in one 128-bit shared load (heap is 16-byte aligned)
-    const ulonglong2 sons = *reinterpret_cast<const ulonglong2*>(heap + j);
-    uint64_t hj = sons.x;
+    // j is even: both sons in one 64-bit shared load (heap is 16-byte aligned)
+    const uint2 sons = *reinterpret_cast<const uint2*>(heap + j);
+    uint32_t hj = sons.x;
     if (j < heap_len) {
-      const uint64_t hj1 = sons.y;
-      if ((hj1 >> 16) <= (hj >> 16)) {
+      const uint32_t hj1 = sons.y;
+      if ((hj1 >> 10) <= (hj >> 10)) {
         j++;
         hj = hj1;
       }
     }
-    if (vk <= (hj >> 16)) break;
+    if (vk <= (hj >> 10)) break;
     heap[k] = hj;
     k = j;
     j <<= 1;
@@ -837,7 +840,7 @@ template <int KIND, int ELEMS>
 __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
   constexpr int max_length = KIND == 2 ? 7 : 15;
   constexpr int base = KIND == 0 ? 257 : 0;
-  uint64_t* heap = s->heap;
+  uint32_t* heap = s->heap;
   int n, max_code = -1, node;
   int heap_len = 0, heap_max = HEAP_SIZE;
   for (n = 0; n < ELEMS; n++) {
@@ -859,10 +862,10 @@ __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
   for (n = heap_len / 2; n >= 1; n--) t_down(heap, heap_len, n);
   node = ELEMS;
   do {
-    const uint64_t en = heap[1];
+    const uint32_t en = heap[1];
     heap[1] = heap[heap_len--];
     t_down(heap, heap_len, 1);
-    const uint64_t em = heap[1];
+    const uint32_t em = heap[1];
     heap[--heap_max] = en;
     heap[--heap_max] = em;
     const uint32_t f = t_freq(en) + t_freq(em);
@@ -882,7 +885,7 @@ __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
     n = t_node(heap[h]);
     bits = t->len[t->dad[n]] + 1;
     if (bits > max_length) bits = max_length, overflow++;
-    t->len[n] = (uint16_t)bits;
+    t->len[n] = (uint8_t)bits;
     if (n > max_code) continue;
     s->bl_count[bits]++;
     int xbits = 0;
@@ -908,7 +911,7 @@ __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
         if (m > max_code) continue;
         if ((uint32_t)t->len[m] != (uint32_t)bits) {
           s->opt_len += ((uint64_t)bits - t->len[m]) * t->freq[m];
-          t->len[m] = (uint16_t)bits;
+          t->len[m] = (uint8_t)bits;
         }
         n--;
       }
@@ -933,7 +936,7 @@ template <int ELEMS>
 __device__ void t_scan_tree(TreesState* s, TreeArr<ELEMS>* t, int max_code) {
   int prevlen = -1, curlen, nextlen = t->len[0], count = 0, max_count = 7, min_count = 4;
   if (nextlen == 0) max_count = 138, min_count = 3;
-  t->len[max_code + 1] = 0xffff;
+  t->len[max_code + 1] = 0xff;
   for (int n = 0; n <= max_code; n++) {
     curlen = nextlen;
     nextlen = t->len[n + 1];
