@@ -1021,7 +1021,10 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   __shared__ TreesState S;
   __shared__ uint32_t hw_buf[HDR_BYTES / 4];
   __shared__ uint32_t s_len_sum, s_last_len, s_hdr_bits;
-  __shared__ uint32_t h_l[L_CODES], h_d[D_CODES];
+  // symbol counts as packed u16 pairs (a block has <= 16383 symbols)
+  __shared__ uint32_t h_l2[(L_CODES + 1) / 2], h_d2[(D_CODES + 1) / 2];
+  auto h_l = [&](int i) -> uint32_t { return (h_l2[i >> 1] >> (16 * (i & 1))) & 0xffff; };
+  auto h_d = [&](int i) -> uint32_t { return (h_d2[i >> 1] >> (16 * (i & 1))) & 0xffff; };
   uint32_t slot = blockIdx.x;
   if (slot >= nblk_slots) return;
   const uint32_t li = blk_lane[slot];
@@ -1037,8 +1040,8 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   const uint32_t nsym = (uint32_t)(s1 - s0);
   // init (init_block: END_BLOCK freq 1)
   for (int i = threadIdx.x; i < (int)BL_CODES; i += blockDim.x) S.blt.freq[i] = 0;
-  for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) h_l[i] = 0;
-  for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) h_d[i] = 0;
+  for (int i = threadIdx.x; i < (int)(L_CODES + 1) / 2; i += blockDim.x) h_l2[i] = 0;
+  for (int i = threadIdx.x; i < (int)(D_CODES + 1) / 2; i += blockDim.x) h_d2[i] = 0;
   for (int i = threadIdx.x; i < (int)(HDR_BYTES / 4); i += blockDim.x) hw_buf[i] = 0;
   if (threadIdx.x == 0) {
     s_len_sum = 0;
@@ -1051,11 +1054,13 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
     if (v & SYM_MATCH) {
       uint32_t lc = v & 0xff, dist = (v >> 8) & 0x7fff;
       local += lc + 3;
-      atomicAdd(&h_l[c_z.length_code[lc] + 257], 1u);
-      atomicAdd(&h_d[d_code(dist)], 1u);
+      const uint32_t li = c_z.length_code[lc] + 257, di = d_code(dist);
+      atomicAdd(&h_l2[li >> 1], 1u << (16 * (li & 1)));
+      atomicAdd(&h_d2[di >> 1], 1u << (16 * (di & 1)));
     } else {
       local += 1;
-      atomicAdd(&h_l[v & 0xff], 1u);
+      const uint32_t li = v & 0xff;
+      atomicAdd(&h_l2[li >> 1], 1u << (16 * (li & 1)));
     }
   };
   {
@@ -1073,8 +1078,8 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   for (int o = 16; o; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(&s_len_sum, local);
   __syncthreads();
-  for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) S.lt.freq[i] = (uint16_t)(h_l[i] + (i == 256));
-  for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) S.dt.freq[i] = (uint16_t)h_d[i];
+  for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) S.lt.freq[i] = (uint16_t)(h_l(i) + (i == 256));
+  for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) S.dt.freq[i] = (uint16_t)h_d(i);
   __syncthreads();
   if (threadIdx.x == 0) {
     S.opt_len = 0;
@@ -1128,14 +1133,14 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   // exact sizes from the symbol histograms (the real counts h_l / h_d, so the
   // frequency-1 nodes build_tree forces into sparse trees are not counted)
   for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) {
-    const uint32_t f = h_l[i];
+    const uint32_t f = h_l(i);
     if (!f) continue;
     const uint32_t x = i >= 257 ? c_extra_lbits[i - 257] : 0;
     dsum += (unsigned long long)f * (S.lt.len[i] + x);
     ssum += (unsigned long long)f * (c_z.sl_len[i] + x);
   }
   for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) {
-    const uint32_t f = h_d[i];
+    const uint32_t f = h_d(i);
     if (!f) continue;
     const uint32_t x = c_extra_dbits[i];
     dsum += (unsigned long long)f * (S.dt.len[i] + x);
