@@ -307,6 +307,83 @@ __global__ void __launch_bounds__(32) k_hash_prev6(const LaneDev* __restrict__ l
   for (int i = lane; i < 32768 * 2 / 16; i += 32) dst[i] = h4[i];
 }
 
+// K3 (current): k_hash_prev6's scan with HP7_W warps sharing one segment and
+// its head table.  Warp w takes tiles w, w + HP7_W, ...: hashing, loads and the
+// in-tile __match_any_sync groups of different tiles proceed in parallel, and
+// only the head-table part of each tile (read heads, then store the tile's last
+// occurrences) runs in tile order, handed from warp to warp by named barriers
+// (the finishing warp arrives, the next one syncs).
+constexpr int HP7_W = 4;
+
+__global__ void __launch_bounds__(32 * HP7_W) k_hash_prev7(const LaneDev* __restrict__ lanes,
+                                                          const WorkItem* __restrict__ work,
+                                                          uint16_t* __restrict__ pd,
+                                                          uint16_t* __restrict__ seg_heads) {
+  extern __shared__ uint16_t hp7_head[];  // position - s + 1 (0 = none)
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + HP4_SEG, n);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint16_t* head = hp7_head;
+  uint4* h4 = reinterpret_cast<uint4*>(head);
+  const uint8_t* src = L.src;
+  uint16_t* out = pd + L.pbase;
+  for (int i = threadIdx.x; i < 32768 * 2 / 16; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+  const uint32_t ntiles = (uint32_t)((e - s + 127) / 128);
+  uint32_t cw = 0, cx = 0;
+  if ((uint32_t)wid < ntiles) hp_load_tile(src, n, s + 128ull * wid, lane, cw, cx);
+  __syncthreads();
+  for (uint32_t t = wid; t < ntiles; t += HP7_W) {
+    const uint64_t c = s + 128ull * t;
+    uint32_t nw = 0, nx = 0;
+    if (t + HP7_W < ntiles) hp_load_tile(src, n, c + 128ull * HP7_W, lane, nw, nx);  // this warp's next tile
+    uint32_t h[4];
+    unsigned peers[4];
+    bool valid[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t q = c + 32 * k + lane;
+      valid[k] = q < e && q + MIN_MATCH <= n;
+      const uint32_t hh = hp_hash_at(cw, cx, k, lane);
+      h[k] = valid[k] ? hh : 0x10000u + lane;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) peers[k] = __match_any_sync(0xffffffffu, h[k]);
+    // wait for tile t - 1's head updates (named barrier: its warp arrives, this one syncs)
+    if (t > 0) asm volatile("bar.sync %0, 64;" ::"r"(1 + (wid + HP7_W - 1) % HP7_W) : "memory");
+    uint32_t d[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t q = c + 32 * k + lane;
+      const unsigned lower = peers[k] & ((1u << lane) - 1);
+      d[k] = 0;
+      if (valid[k]) {
+        if (lower) {
+          d[k] = lane - (31 - __clz(lower));
+        } else {
+          const uint32_t r = head[h[k]];
+          d[k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
+        }
+      }
+      __syncwarp();
+      if (valid[k] && (peers[k] >> lane) == 1u) head[h[k]] = (uint16_t)(q - s + 1);
+      __syncwarp();
+    }
+    if (t + 1 < ntiles) asm volatile("bar.arrive %0, 64;" ::"r"(1 + wid) : "memory");
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t q = c + 32 * k + lane;
+      if (q < e) out[q] = (uint16_t)d[k];
+    }
+    cw = nw, cx = nx;
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)blockIdx.x * 32768);
+  for (int i = threadIdx.x; i < 32768 * 2 / 16; i += blockDim.x) dst[i] = h4[i];
+}
+
 // k_hash_fix2: one CTA per segment, eight positions per thread and step
 // (one 16-byte load of their links); only positions marked 0xffff compute their
 // hash and read the previous segment's final head table.
@@ -379,7 +456,11 @@ static int hash_prev_two_phase(Workspace& sortws, Workspace& W, const LaneDev* d
   BB_CUDA_TRY(cudaMemcpyAsync(d_work, work.data(), sizeof(WorkItem) * work.size(), cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_seg0, seg0.data(), 4 * nl, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
-  k_hash_prev6<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
+  static const bool k3_single = getenv("BB_K3_SINGLE_WARP") != nullptr;
+  if (k3_single)
+    k_hash_prev6<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
+  else
+    k_hash_prev7<<<(unsigned)work.size(), 32 * HP7_W, 65536, st>>>(d_lanes, d_work, d_pd, heads);
   BB_LAUNCH_CHECK();
   k_hash_fix2<<<(unsigned)work.size(), 256, 0, st>>>(d_lanes, d_work, d_pd, heads);
   BB_LAUNCH_CHECK();
@@ -1620,6 +1701,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     ZTables t = make_tables();
     BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev7, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
     e->tables_ready = true;
   }
@@ -1858,6 +1940,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   ZTables t = make_tables();
   BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev7, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
   LaneDev d{};
   d.src = d_in;
