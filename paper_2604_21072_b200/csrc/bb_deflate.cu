@@ -1736,7 +1736,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     d.src = j.src;
     d.n = j.n;
     d.pbase = pos_total;
-    d.G = j.n <= (4u << 20) ? 2048 : 4096;
+    d.G = j.n <= (1u << 20) ? 256 : j.n <= (4u << 20) ? 1024 : 4096;  // small lanes: more, shorter parse segments
     d.seg0 = seg_total;
     d.nseg = (uint32_t)std::max<uint64_t>(1, (j.n + d.G - 1) / d.G);
     d.blk0 = blk_total;
