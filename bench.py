@@ -44,6 +44,7 @@ SD_REQUESTS, SD_NODES, SD_DIM, SD_KEEP_PCT = 32, 64 * 8, 4096, 60
 KV_BATCH, KV_CTX, KV_DIM, KV_GROUP = 32, 4096, 5120, 16
 SWEEP_DIM = 8192
 MiB = 1 << 20
+HANDOFF = "p2p"  # multi-GPU hand-off of config1/2 frames: "p2p" (fused into the codec) or "nccl"
 
 
 def _threads(fn, n):
@@ -113,6 +114,18 @@ class ActWorkload(Workload):
         self.rank, self.world = rank, world
 
     def step(self, ring, step_no):
+        if ring is not None and HANDOFF == "p2p":
+            # fused hand-off: the compress pipeline writes the frames into the next GPU's inbox
+            from paper_2604_21072_b200.pipeline import (FLAG_BYTE_SPLIT, FLAG_COMPRESSED, PeerInbox,
+                                                        open_frames)
+            if getattr(self, "peer", None) is None:
+                self.peer = PeerInbox([o.numel() for o in self.outs], self.xs[0].device)
+            ptrs, caps = self.peer.out_ptrs(step_no)
+            lens = self.dc.compress_batch_ptr(self.xs, ptrs, caps)
+            frames = self.peer.post(step_no, lens, step_no, FLAG_COMPRESSED | FLAG_BYTE_SPLIT)
+            _, cs = open_frames(frames)
+            self.dc.decompress_batch(cs, self.decs)
+            return sum(lens)
         lens = self.dc.compress_batch(self.xs, self.outs)
         cs = [o[:n] for o, n in zip(self.outs, lens)]
         if ring is not None:
@@ -541,7 +554,11 @@ def main():
     ap.add_argument("--sweep-max-mib", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--handoff", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: frames written into the next GPU by the codec (p2p) or sent by NCCL")
     args = ap.parse_args()
+    global HANDOFF
+    HANDOFF = args.handoff
     world, rank, local = dist_init()
     if args.impl == "reference":
         if args.workload == "config5":
@@ -716,7 +733,9 @@ def main():
                    "l2": f"inputs {raw_step / MiB:.0f} MiB/step > 126 MB L2 (no flush needed)"
                    if raw_step > 126e6 else "inputs smaller than L2",
                    "parallelism": f"{world} stage(s), one boundary per GPU"
-                   + (", BBF1 frames over NVLink (NCCL P2P ring)" if world > 1 else "")},
+                   + ((", BBF1 frames written into the next GPU's HBM by the codec over NVLink (CUDA IPC),"
+                       " lengths by NCCL" if HANDOFF == "p2p" and isinstance(wl, ActWorkload)
+                       else ", BBF1 frames over NVLink (NCCL P2P ring)") if world > 1 else "")},
         "lossless": ok, "bit_exact_vs_reference": bit_exact,
         "tokens_per_s": world * wl.tokens_per_step / (ms_step / 1e3),
         "pipeline_tokens_per_s": wl.tokens_per_step / (ms_step / 1e3),

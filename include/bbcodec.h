@@ -135,6 +135,18 @@ BB_API int bb_unpack_sd(const uint8_t* d_in, size_t n, size_t hidden_dim, uint32
 BB_API int bb_gather_pages(const uint8_t* d_pool, size_t n_pool_pages, size_t page_bytes,
                            const uint32_t* d_page_ids, uint32_t n_pages, uint8_t* d_out, void* stream);
 
+/* ---- multi-GPU hand-off ------------------------------------------------ */
+/* Lets kernels running on `device` read / write memory of `peer` over NVLink (the
+ * codec then writes its containers straight into the next stage's HBM). */
+BB_API int bb_enable_peer_access(int device, int peer);
+/* CUDA IPC: export a device pointer as (64-byte handle of its allocation, offset); import it
+ * into `device`'s context (the stage that writes into it); close with the returned base. */
+BB_API int bb_ipc_export(const void* d_ptr, void* handle64, size_t* offset);
+BB_API int bb_ipc_import(int device, const void* handle64, size_t offset, void** d_ptr, void** d_base);
+BB_API int bb_ipc_close(void* d_base);
+/* stream-ordered host -> device copy (e.g. frame headers into a peer's inbox) */
+BB_API int bb_copy_h2d(void* d_dst, const void* h_src, size_t n, void* stream);
+
 /* ---- instrumentation ---------------------------------------------------- */
 /* Number of kernels this library launched (process-wide, monotonic). */
 BB_API uint64_t bb_kernel_launches(void);

@@ -23,7 +23,8 @@ EXPORTS = [
     "bb_compress_host", "bb_decompress_host", "bb_backend_encode_host", "bb_backend_decode_host",
     "bb_split_host", "bb_merge_host", "bb_histogram256_host", "bb_kernel_launches",
     "bb_stage_timing", "bb_stage_report", "bb_packed_bound", "bb_pack_sd", "bb_unpack_sd",
-    "bb_gather_pages",
+    "bb_gather_pages", "bb_enable_peer_access", "bb_ipc_export", "bb_ipc_import", "bb_ipc_close",
+    "bb_copy_h2d",
 ]
 
 _u8p = C.c_void_p
@@ -79,6 +80,11 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         L.bb_unpack_sd.argtypes = [_u8p, _sz, _sz, C.POINTER(C.c_uint32), _sz, C.POINTER(C.c_uint32),
                                    _szp, C.c_void_p]
         L.bb_gather_pages.argtypes = [_u8p, _sz, _sz, _u8p, C.c_uint32, _u8p, C.c_void_p]
+        L.bb_enable_peer_access.argtypes = [C.c_int, C.c_int]
+        L.bb_ipc_export.argtypes = [_u8p, C.c_void_p, _szp]
+        L.bb_ipc_import.argtypes = [C.c_int, C.c_void_p, _sz, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+        L.bb_ipc_close.argtypes = [C.c_void_p]
+        L.bb_copy_h2d.argtypes = [C.c_void_p, C.c_void_p, _sz, C.c_void_p]
         L.bb_kernel_launches.restype = C.c_uint64
         L.bb_stage_timing.argtypes = [C.c_int]
         L.bb_stage_report.restype = C.c_char_p

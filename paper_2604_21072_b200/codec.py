@@ -339,6 +339,20 @@ class DeviceCodec:
                                         st, self._stream(stream)))
         return list(lens)
 
+    def compress_batch_ptr(self, xs, out_ptrs, out_caps, backend: int = kBackendDeflate, split: bool = True,
+                           stream=None) -> List[int]:
+        """compress_batch into raw device addresses (e.g. the next stage's inbox mapped by CUDA IPC)."""
+        k = len(xs)
+        ins = (C.c_void_p * k)(*[x.data_ptr() for x in xs])
+        ns = (C.c_size_t * k)(*[x.numel() for x in xs])
+        os_ = (C.c_void_p * k)(*[int(p) for p in out_ptrs])
+        caps = (C.c_size_t * k)(*[int(c) for c in out_caps])
+        lens = (C.c_size_t * k)()
+        st = (C.c_int * k)()
+        _check(self.L.bb_compress_batch(self.ctx, k, ins, ns, backend, int(split), os_, caps, lens,
+                                        st, self._stream(stream)))
+        return list(lens)
+
     def decoded_size(self, c, stream=None) -> int:
         n = C.c_size_t()
         _check(self.L.bb_decompress(self.ctx, c.data_ptr(), c.numel(), None, 0, C.byref(n),

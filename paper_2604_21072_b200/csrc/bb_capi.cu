@@ -17,6 +17,10 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
+#include <cstring>
+
 #include "bb_common.cuh"
 #include "bb_kernels.h"
 
@@ -184,6 +188,88 @@ extern "C" {
 
 const char* bb_last_error(void) { return t_err.c_str(); }
 const char* bb_version(void) { return "bbcodec-b200 0.1 (sm_100a)"; }
+int bb_enable_peer_access(int device, int peer) {
+  int cur = 0;
+  BB_CUDA_TRY(cudaGetDevice(&cur));
+  BB_CUDA_TRY(cudaSetDevice(device));
+  int can = 0;
+  cudaError_t e = cudaDeviceCanAccessPeer(&can, device, peer);
+  if (e == cudaSuccess && can) {
+    e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+      cudaGetLastError();
+      e = cudaSuccess;
+    }
+  } else if (e == cudaSuccess) {
+    e = cudaErrorPeerAccessUnsupported;
+  }
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) {
+    bb::set_error("peer access %d -> %d: %s", device, peer, cudaGetErrorString(e));
+    return BB_CUDA_ERROR;
+  }
+  return BB_OK;
+}
+
+// CUDA IPC for the direct hand-off: a device pointer (possibly inside a larger
+// allocation of a caching allocator) is exported as (handle of its allocation,
+// offset) and imported into the *caller's* device context, so kernels of this
+// stage can write the next stage's HBM over NVLink.
+int bb_ipc_export(const void* d_ptr, void* handle64, size_t* offset) {
+  if (!d_ptr || !handle64 || !offset) {
+    bb::set_error("ipc_export: null argument");
+    return BB_INVALID_ARG;
+  }
+  // the driver's cuMemGetAddressRange, fetched through the runtime (no libcuda link
+  // dependency, so the library still loads on machines without a driver)
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    BB_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      bb::set_error("ipc_export: cuMemGetAddressRange unavailable");
+      return BB_CUDA_ERROR;
+    }
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
+    bb::set_error("ipc_export: cuMemGetAddressRange failed");
+    return BB_CUDA_ERROR;
+  }
+  BB_CUDA_TRY(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle64), reinterpret_cast<void*>(base)));
+  *offset = reinterpret_cast<uintptr_t>(d_ptr) - (uintptr_t)base;
+  return BB_OK;
+}
+
+int bb_ipc_import(int device, const void* handle64, size_t offset, void** d_ptr, void** d_base) {
+  if (!handle64 || !d_ptr || !d_base) {
+    bb::set_error("ipc_import: null argument");
+    return BB_INVALID_ARG;
+  }
+  BB_CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  void* base = nullptr;
+  BB_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *d_base = base;
+  *d_ptr = static_cast<char*>(base) + offset;
+  return BB_OK;
+}
+
+int bb_ipc_close(void* d_base) {
+  BB_CUDA_TRY(cudaIpcCloseMemHandle(d_base));
+  return BB_OK;
+}
+
+int bb_copy_h2d(void* d_dst, const void* h_src, size_t n, void* stream) {
+  BB_CUDA_TRY(cudaMemcpyAsync(d_dst, h_src, n, cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream)));
+  return BB_OK;
+}
+
 uint64_t bb_kernel_launches(void) { return g_launches.load(); }
 
 void bb_stage_timing(int enable) { g_stage_timing.store(enable); }

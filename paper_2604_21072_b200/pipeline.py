@@ -195,6 +195,88 @@ class StageRing:
         return out
 
 
+class PeerInbox:
+    """Direct stage-to-stage hand-off over NVLink.
+
+    Each stage allocates `slots` inbox buffers in its own HBM; the previous stage
+    imports them into its device context (CUDA IPC, include/bbcodec.h
+    bb_ipc_export / bb_ipc_import), so the codec's final kernels (bit emission,
+    container header) write the compressed frames straight into the receiving
+    GPU's memory over NVLink -- the transfer is fused into the compress pipeline
+    instead of a separate NCCL copy.  Only the frame lengths go through NCCL P2P:
+    a small "doorbell" that also orders buffer reuse (slot k % slots is rewritten
+    only after the receiver has posted the doorbell of the step after k, i.e.
+    finished decoding k).  Frame m of a step sits at a fixed offset: 20-byte BBF1
+    header, then the container."""
+
+    def __init__(self, caps, device, slots: int = 2):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        from .codec import _check
+        self.C, self.torch, self.dist, self._check = C, torch, dist, _check
+        self.L = _lib.load()
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.next, self.prev = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        self.device = device
+        self.offsets, off = [], 0
+        for c in caps:
+            self.offsets.append(off)
+            off = (off + FRAME_HEADER + int(c) + 255) & ~255
+        self.slot_bytes = off
+        self.slots = slots
+        self.caps = [int(c) for c in caps]
+        self.inbox = [torch.empty(self.slot_bytes, dtype=torch.uint8, device=device) for _ in range(slots)]
+        exported = []
+        for b in self.inbox:
+            h = (C.c_uint8 * 64)()
+            o = C.c_size_t()
+            _check(self.L.bb_ipc_export(b.data_ptr(), h, C.byref(o)))
+            exported.append((bytes(h), o.value))
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, exported)
+        self.out_base, self.out_ptr = [], []
+        for hb, o in gathered[self.next]:
+            p, base = C.c_void_p(), C.c_void_p()
+            hbuf = (C.c_uint8 * 64).from_buffer_copy(hb)
+            _check(self.L.bb_ipc_import(device.index, hbuf, o, C.byref(p), C.byref(base)))
+            self.out_ptr.append(p.value)
+            self.out_base.append(base.value)
+        torch.cuda.set_device(device)
+
+    def out_ptrs(self, slot: int):
+        """Container destinations inside the next stage's inbox (after each frame header)."""
+        base = self.out_ptr[slot % self.slots]
+        return [base + o + FRAME_HEADER for o in self.offsets], self.caps
+
+    def post(self, slot: int, lens, batch_id: int, flags: int, msg_type: int = T_ACTIVATIONS):
+        """Write the frame headers next to the containers already in the peer's inbox and
+        exchange lengths with both neighbours; returns the previous stage's frames (views
+        of this stage's inbox)."""
+        C, torch, dist = self.C, self.torch, self.dist
+        stream = torch.cuda.current_stream(self.device)
+        base = self.out_ptr[slot % self.slots]
+        hdrs = [frame_header(msg_type, batch_id, m, flags, int(n)) for m, n in enumerate(lens)]
+        for o, h in zip(self.offsets, hdrs):
+            self._check(self.L.bb_copy_h2d(base + o, h, FRAME_HEADER, stream.cuda_stream))
+        stream.synchronize()  # containers + headers are in the peer's HBM
+        out = torch.tensor([int(n) for n in lens], dtype=torch.int64, device=self.device)
+        got = torch.empty(len(lens), dtype=torch.int64, device=self.device)
+        for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, out, self.next),
+                                         dist.P2POp(dist.irecv, got, self.prev)]):
+            r.wait()
+        ib = self.inbox[slot % self.slots]
+        return [ib[o:o + FRAME_HEADER + int(n)] for o, n in zip(self.offsets, got.tolist())]
+
+    def close(self):
+        for b in self.out_base:
+            self.L.bb_ipc_close(b)
+        self.out_base, self.out_ptr = [], []
+
+
 def build_frames(containers, batch_id: int, flags: int, device, msg_type: int = T_ACTIVATIONS):
     """BBF1 frames on the device: host-built 20-byte headers + container bytes
     (msg_type T_PACKED_SD for speculative-decoding token-tree payloads)."""
