@@ -528,16 +528,40 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
   const uint8_t* src = L.src;
   const uint16_t* pdl = pd + L.pbase;
   if (threadIdx.x == 0) w32[0] = 0;
-  for (uint32_t i = threadIdx.x; i < wlen; i += blockDim.x) {
-    const uint64_t q = wlo + i;
-    uint32_t v = 0;
-    if (q < e) {
-      const uint32_t l = pdl[q];
-      if (l && l <= i) v = i - l + 1;  // 1-based index of the predecessor inside the window
+  {
+    // four window positions per thread: one 8-byte load of their links, two 4-byte
+    // loads of their bytes (wlo, the lane bases and the link array are 4-aligned)
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(pdl)) & 7) == 0;
+    const uint32_t nq = (wlen + 3) / 4;
+    for (uint32_t j = threadIdx.x; j < nq; j += blockDim.x) {
+      const uint32_t i0 = 4 * j;
+      const uint64_t q0 = wlo + i0;
+      if (aligned && q0 + 4 <= e && q0 + 8 <= n) {
+        const uint2 l4 = __ldg(reinterpret_cast<const uint2*>(pdl + q0));
+        const uint32_t b0 = __ldg(reinterpret_cast<const uint32_t*>(src + q0));
+        const uint32_t b1 = __ldg(reinterpret_cast<const uint32_t*>(src + q0 + 4));
+        const uint32_t ls[4] = {l4.x & 0xffff, l4.x >> 16, l4.y & 0xffff, l4.y >> 16};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const uint32_t i = i0 + k, l = ls[k];
+          uint32_t v = (l && l <= i) ? i - l + 1 : 0;                    // 1-based predecessor index
+          v |= __byte_perm(b0, b1, (k | ((k + 1) << 4)) & 0xff) << 16;  // bytes q, q + 1
+          w32[i + 1] = v;
+        }
+      } else {
+        for (uint32_t i = i0; i < i0 + 4 && i < wlen; i++) {
+          const uint64_t q = wlo + i;
+          uint32_t v = 0;
+          if (q < e) {
+            const uint32_t l = pdl[q];
+            if (l && l <= i) v = i - l + 1;
+          }
+          if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
+          if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
+          w32[i + 1] = v;
+        }
+      }
     }
-    if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
-    if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
-    w32[i + 1] = v;
   }
   __syncthreads();
   const char* wb = reinterpret_cast<const char*>(w32);
