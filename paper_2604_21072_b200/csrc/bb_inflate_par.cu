@@ -1432,6 +1432,22 @@ struct ExtEntry {
   uint32_t src;
 };
 
+// window entries <- RESOLVED | byte, 16 bytes per 128-bit load where aligned
+__device__ __forceinline__ void fill_entries(uint32_t* ent, const uint8_t* src, uint32_t w, uint32_t total) {
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const uint32_t nv = w / 16;
+    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(src) + v);
+      const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < 16; k++) ent[16 * v + k] = RESOLVED | ((wd[k >> 2] >> (8 * (k & 3))) & 0xff);
+    }
+    for (uint32_t i = 16 * nv + threadIdx.x; i < total; i += blockDim.x) ent[i] = RESOLVED | (i < w ? src[i] : 0u);
+  } else {
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) ent[i] = RESOLVED | (i < w ? src[i] : 0u);
+  }
+}
+
 __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __restrict__ jobs,
                                                               const uint32_t* __restrict__ job_of_sub,
                                                               const uint64_t* __restrict__ out_total,
@@ -1464,7 +1480,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
     return;
   }
   if (threadIdx.x == 0) wflag[blockIdx.x] = 1;
-  for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) ent[i] = RESOLVED | J.dst[S + i];
+  fill_entries(ent, J.dst + S, W, W);
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   __shared__ int corrupt;
@@ -1573,7 +1589,7 @@ __global__ void __cluster_dims__(RS_CL, 1, 1) __launch_bounds__(RS_THREADS)
     cl.sync();  // rank 0's flag is read by all before anyone exits
     return;
   }
-  for (uint32_t i = threadIdx.x; i < SUB; i += blockDim.x) ent[i] = RESOLVED | (i < Wn ? J.dst[S + i] : 0u);
+  fill_entries(ent, J.dst + S, Wn, SUB);
   __syncthreads();
   if (has_m) {
     for (uint64_t k = m0 + threadIdx.x; k < nm && M[k].dst < S + Wn; k += blockDim.x) {
