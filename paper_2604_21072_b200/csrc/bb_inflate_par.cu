@@ -445,15 +445,17 @@ __global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __r
   const uint64_t T = (blockIdx.x - blk_prefix[j]) * 256ull + threadIdx.x;  // bytes [4T, 4T + 4)
   const uint64_t B0 = 4 * T;
   const int lane = threadIdx.x & 31;
-  uint32_t dbits = 0, sbits = 0;
-  if (B0 < J.n) {
-    const uint64_t nbits = 8 * J.n;
-    if (find_dynamic) {
-      const uint64_t x0 = peek64(J.src, J.n, 8 * B0), x1 = peek64(J.src, J.n, 8 * B0 + 64);
+  uint32_t sbits = 0;
+  if (find_dynamic) {
+    uint32_t cm = 0;
+    uint64_t x0 = 0, x1 = 0;
+    if (B0 < J.n) {
+      const uint64_t nbits = 8 * J.n;
+      x0 = peek64(J.src, J.n, 8 * B0), x1 = peek64(J.src, J.n, 8 * B0 + 64);
       uint64_t m = ~(x0 >> 1) & (x0 >> 2);
       m &= ~((x0 >> 4) & (x0 >> 5) & (x0 >> 6) & (x0 >> 7));
       m &= ~((x0 >> 9) & (x0 >> 10) & (x0 >> 11) & (x0 >> 12));
-      uint32_t cm = (uint32_t)m;
+      cm = (uint32_t)m;
       // stream limits: b >= 16 and b + 17 <= 8 n
       const uint64_t b0 = 8 * B0;
       if (b0 < 16) cm &= 0xffffffffu << (uint32_t)(16 - b0);
@@ -461,18 +463,62 @@ __global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __r
         const int64_t keep = (int64_t)nbits - 17 - (int64_t)b0 + 1;  // offsets i < keep are allowed
         cm &= keep <= 0 ? 0u : (keep >= 32 ? 0xffffffffu : ((1u << keep) - 1));
       }
-      while (cm) {
-        const uint32_t i = __ffs(cm) - 1;
-        cm &= cm - 1;
-        const uint32_t ncode = bits_at(x0, x1, i + 13, 4) + 4;
+    }
+    // the warp's survivors are dealt out one per lane (the Kraft check of the
+    // code-length code runs with every lane busy instead of per-lane loops)
+    const uint32_t cnt = __popc(cm);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t x0lo = (uint32_t)x0, x0hi = (uint32_t)(x0 >> 32), x1lo = (uint32_t)x1, x1hi = (uint32_t)(x1 >> 32);
+    for (uint32_t base = 0; base < tot; base += 32) {
+      const uint32_t k = base + lane;
+      // owner: the first lane whose inclusive count exceeds k (binary search over lanes)
+      int owner = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+        if (v <= k) owner += step;
+      }
+      const uint32_t oinc = __shfl_sync(0xffffffffu, incl, owner);
+      const uint32_t ocnt = __shfl_sync(0xffffffffu, cnt, owner);
+      const uint32_t ocm = __shfl_sync(0xffffffffu, cm, owner);
+      const uint64_t wx0 = (uint64_t)__shfl_sync(0xffffffffu, x0lo, owner) |
+                           ((uint64_t)__shfl_sync(0xffffffffu, x0hi, owner) << 32);
+      const uint64_t wx1 = (uint64_t)__shfl_sync(0xffffffffu, x1lo, owner) |
+                           ((uint64_t)__shfl_sync(0xffffffffu, x1hi, owner) << 32);
+      bool pass = false;
+      uint32_t i = 0;
+      if (k < tot) {
+        const uint32_t slot = k - (oinc - ocnt);
+        i = __fns(ocm, 0, (int)slot + 1);
+        const uint32_t ncode = bits_at(wx0, wx1, i + 13, 4) + 4;
         uint32_t kraft = 0;
-        for (uint32_t k = 0; k < ncode && kraft <= 128; k++) {
-          const uint32_t l = bits_at(x0, x1, i + 17 + 3 * k, 3);
+        for (uint32_t kk = 0; kk < ncode && kraft <= 128; kk++) {
+          const uint32_t l = bits_at(wx0, wx1, i + 17 + 3 * kk, 3);
           kraft += l ? (128u >> l) : 0u;
         }
-        if (kraft == 128) dbits |= 1u << i;
+        pass = kraft == 128;
+      }
+      // warp-aggregated append of the round's survivors
+      const unsigned bal = __ballot_sync(0xffffffffu, pass);
+      if (bal) {
+        unsigned long long sbase = 0;
+        if (lane == 0) sbase = atomicAdd(surv_cnt, (unsigned long long)__popc(bal));
+        sbase = __shfl_sync(0xffffffffu, sbase, 0);
+        if (pass) {
+          const uint64_t slot = sbase + __popc(bal & ((1u << lane) - 1));
+          const uint64_t ob0 = B0 - 4ull * (uint64_t)(lane - owner);  // owner's first byte
+          if (slot < surv_cap) surv[slot] = ((uint64_t)j << 48) | (8 * ob0 + i);
+        }
       }
     }
+  }
+  if (B0 < J.n) {
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       const uint64_t B = B0 + k;
@@ -482,21 +528,6 @@ __global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __r
         if (len == (~nlen & 0xffff) && B + 4 + len <= J.n) sbits |= 1u << k;
       }
     }
-  }
-  {
-    const uint32_t cnt = __popc(dbits);
-    uint32_t pre = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += v;
-    }
-    const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
-    unsigned long long base = 0;
-    if (lane == 0 && tot) base = atomicAdd(surv_cnt, (unsigned long long)tot);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    uint64_t slot = base + pre - cnt;
-    for (uint32_t v = dbits; v; v &= v - 1, slot++)
-      if (slot < surv_cap) surv[slot] = ((uint64_t)j << 48) | (8 * B0 + (__ffs(v) - 1));
   }
   // stored bitmap: 8 lanes (32 bytes) per word
   uint32_t wv = sbits << (4 * (lane & 7));
