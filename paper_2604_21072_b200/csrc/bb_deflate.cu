@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     }
   }
   __syncthreads();
-  const char* wb = reinterpret_cast<const char*>(w32);
+  const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w32);
 
   for (uint64_t p0 = s; p0 < e; p0 += blockDim.x) {
     const uint64_t p = p0 + threadIdx.x;
@@ -574,7 +574,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     const uint32_t d0 = ip1 - c0;
     const bool live = p < e && p + MIN_MATCH <= n && c0 != 0 && d0 <= MAX_DIST && wlo + c0 - 1 != 0;
     uint32_t best = MIN_MATCH - 1, bestd = 0, flag = 0, nice = 0, maxl = 0, lim1 = 0;
-    uint32_t ic1 = 0, key = PF_DEAD_KEY, off = 4 * (MIN_MATCH - 2) + 2;
+    // ic4: 4 x the candidate's 1-based window index (byte offset of its word)
+    uint32_t ic4 = 0, key = PF_DEAD_KEY, offb = sw + 4 * (MIN_MATCH - 2) + 2;
     if (live) {
       const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
       nice = min(NICE_LENGTH, la);
@@ -582,9 +583,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
       const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
       lim1 = limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0;
       flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
-      ic1 = c0;
+      ic4 = 4 * c0;
       key = (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u);
     }
+    const uint32_t lim4 = 4 * lim1;
     // one batch of B chain steps, then the recorded candidates in chain order
     auto batch = [&](auto bsize) {
       constexpr int B = decltype(bsize)::value;
@@ -592,21 +594,21 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
       uint32_t mask = 0;
 #pragma unroll
       for (int t = 0; t < B; t++) {
-        const uint32_t wc = *reinterpret_cast<const uint32_t*>(wb + 4 * ic1);
-        const uint32_t we = *reinterpret_cast<const uint16_t*>(wb + 4 * ic1 + off);
-        cand[t] = ic1;
-        mask |= __byte_perm(wc, we, 0x5432) == key ? 1u << t : 0u;
-        const uint32_t nx = wc & 0xffff;
-        const bool end = nx <= lim1;
-        ic1 = end ? 0 : nx;
-        key = end ? PF_DEAD_KEY : key;
+        // past the distance limit (or at the sentinel, which links to itself) a
+        // candidate is walked but never recorded: chains only go backwards
+        uint32_t wc, we;  // the candidate's word; bytes (best - 1, best) of the candidate
+        asm("ld.shared.u32 %0, [%1];" : "=r"(wc) : "r"(sw + ic4));
+        asm("ld.shared.u16 %0, [%1];" : "=r"(we) : "r"(ic4 + offb));
+        cand[t] = ic4;
+        mask |= (__byte_perm(wc, we, 0x5432) == key && ic4 > lim4) ? 1u << t : 0u;
+        ic4 = (wc << 2) & 0x3fffc;
       }
       if (__any_sync(0xffffffffu, mask != 0)) {
         bool improved = false;
         while (mask) {
           const int t = __ffs(mask) - 1;
           mask &= mask - 1;
-          const uint32_t c = pf_pick(cand, t);
+          const uint32_t c = pf_pick(cand, t) >> 2;
           // re-test only if best grew in this flush (else it is the test the step already made)
           if (improved && (((w32[c] ^ wp) | (w32[c + best - 1] ^ w32[ip1 + best - 1])) & 0xffff0000u) != 0)
             continue;
@@ -626,23 +628,23 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
             improved = true;
             if (len >= nice) {
               mask = 0;
-              ic1 = 0;
+              ic4 = 0;
             }
           }
         }
         if (improved) {
-          off = 4 * (best - 1) + 2;
-          key = ic1 ? (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u) : PF_DEAD_KEY;
+          offb = sw + 4 * (best - 1) + 2;
+          key = (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u);
         }
       }
     };
     for (int cnt = 0; cnt < 32; cnt += PF_B1) {
-      if (!__any_sync(0xffffffffu, ic1 != 0)) break;
+      if (!__any_sync(0xffffffffu, ic4 > lim4)) break;
       batch(std::integral_constant<int, PF_B1>());
     }
     const uint32_t r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
     for (int cnt = 32; cnt < (int)MAX_CHAIN; cnt += PF_B2) {
-      if (!__any_sync(0xffffffffu, ic1 != 0)) break;
+      if (!__any_sync(0xffffffffu, ic4 > lim4)) break;
       batch(std::integral_constant<int, PF_B2>());
     }
     if (p < e) prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, live ? r32 | flag : 0);
