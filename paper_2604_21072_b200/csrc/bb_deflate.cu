@@ -533,33 +533,57 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     // loads of their bytes (wlo, the lane bases and the link array are 4-aligned)
     const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(pdl)) & 7) == 0;
     const uint32_t nq = (wlen + 3) / 4;
-    for (uint32_t j = threadIdx.x; j < nq; j += blockDim.x) {
-      const uint32_t i0 = 4 * j;
-      const uint64_t q0 = wlo + i0;
-      if (aligned && q0 + 4 <= e && q0 + 8 <= n) {
-        const uint2 l4 = __ldg(reinterpret_cast<const uint2*>(pdl + q0));
-        const uint32_t b0 = __ldg(reinterpret_cast<const uint32_t*>(src + q0));
-        const uint32_t b1 = __ldg(reinterpret_cast<const uint32_t*>(src + q0 + 4));
-        const uint32_t ls[4] = {l4.x & 0xffff, l4.x >> 16, l4.y & 0xffff, l4.y >> 16};
+    // groups j < jf take the vector path (q0 + 4 <= e, q0 + 8 <= n); their loads are
+    // issued PF_STAGE_U groups at a time so several L2 round trips are in flight
+    uint32_t jf = 0;
+    if (aligned) {
+      const uint64_t lim = umin64(e >= 4 ? e - 4 : 0, n >= 8 ? n - 8 : 0);
+      jf = lim >= wlo ? (uint32_t)umin64((lim - wlo) / 4 + 1, nq) : 0;
+    }
+    constexpr int U = 4;
+    for (uint32_t j0 = threadIdx.x; j0 < jf; j0 += U * blockDim.x) {
+      uint2 l4[U];
+      uint32_t b0[U], b1[U];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-          const uint32_t i = i0 + k, l = ls[k];
-          uint32_t v = (l && l <= i) ? i - l + 1 : 0;                    // 1-based predecessor index
-          v |= __byte_perm(b0, b1, (k | ((k + 1) << 4)) & 0xff) << 16;  // bytes q, q + 1
-          w32[i + 1] = v;
+      for (int u = 0; u < U; u++) {
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j < jf) {
+          const uint64_t q0 = wlo + 4 * j;
+          l4[u] = __ldg(reinterpret_cast<const uint2*>(pdl + q0));
+          b0[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0));
+          b1[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0 + 4));
         }
-      } else {
-        for (uint32_t i = i0; i < i0 + 4 && i < wlen; i++) {
-          const uint64_t q = wlo + i;
-          uint32_t v = 0;
-          if (q < e) {
-            const uint32_t l = pdl[q];
-            if (l && l <= i) v = i - l + 1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j < jf) {
+          const uint32_t i0 = 4 * j;
+          const uint32_t ls[4] = {l4[u].x & 0xffff, l4[u].x >> 16, l4[u].y & 0xffff, l4[u].y >> 16};
+          uint32_t v[4];
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const uint32_t i = i0 + k, l = ls[k];
+            v[k] = (l && l <= i) ? i - l + 1 : 0;                                 // 1-based predecessor index
+            v[k] |= __byte_perm(b0[u], b1[u], (k | ((k + 1) << 4)) & 0xff) << 16;  // bytes q, q + 1
           }
-          if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
-          if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
-          w32[i + 1] = v;
+#pragma unroll
+          for (int k = 0; k < 4; k++) w32[i0 + k + 1] = v[k];
         }
+      }
+    }
+    for (uint32_t j = jf + threadIdx.x; j < nq; j += blockDim.x) {
+      const uint32_t i0 = 4 * j;
+      for (uint32_t i = i0; i < i0 + 4 && i < wlen; i++) {
+        const uint64_t q = wlo + i;
+        uint32_t v = 0;
+        if (q < e) {
+          const uint32_t l = pdl[q];
+          if (l && l <= i) v = i - l + 1;
+        }
+        if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
+        if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
+        w32[i + 1] = v;
       }
     }
   }
