@@ -685,15 +685,19 @@ def main():
         t_launch = per_launch[dom] / 1e3
         a_bytes = alg.get(dom, (raw_step + comp_step) // n_launch)
         achieved = a_bytes / t_launch / 1e9
-        traffic = None
+        traffic = limiter = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                traffic = json.load(f).get(wl.name, {}).get(dom)
+                tj = json.load(f)
+            traffic = tj.get(wl.name, {}).get(dom)
+            limiter = tj.get("limiters", {}).get(wl.name, {}).get(dom)
         except OSError:
             pass
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": a_bytes,
                 "launch_ms": per_launch[dom], "peak_source": peak_src}
+        if limiter:  # the on-chip resource the kernel actually saturates (from the committed ncu capture)
+            roof["limiter"] = limiter
     codec_roof = 2 * (raw_step + comp_step) / (ms_step / 1e3) / 1e9
 
     cpu = None
