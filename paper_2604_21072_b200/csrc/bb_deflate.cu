@@ -516,7 +516,7 @@ constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;
 __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __restrict__ lanes,
                                                             const WorkItem* __restrict__ work,
                                                             const uint16_t* __restrict__ pd,
-                                                            uint2* __restrict__ prof) {
+                                                            uint2* __restrict__ prof, int with_bytes) {
   extern __shared__ __align__(16) uint32_t w32[];
   const WorkItem w = work[blockIdx.x];
   const LaneDev L = lanes[w.lane];
@@ -610,7 +610,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
       ic4 = 4 * c0;
       key = (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u);
     }
-    const uint32_t lim4 = 4 * lim1;
+    // zlib tests the limit only from the second candidate on (do ... while (prev > limit)):
+    // a head exactly at MAX_DIST is still compared, and every later candidate is below it
+    const uint32_t lim4 = 4 * lim1 - (live && c0 == lim1 ? 4u : 0u);
     // one batch of B chain steps, then the recorded candidates in chain order
     auto batch = [&](auto bsize) {
       constexpr int B = decltype(bsize)::value;
@@ -671,27 +673,62 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
       if (!__any_sync(0xffffffffu, ic4 > lim4)) break;
       batch(std::integral_constant<int, PF_B2>());
     }
-    if (p < e) prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, live ? r32 | flag : 0);
+    if (p < e) {
+      // y: the 32-chain profile (the flag lives in x) | the byte before p << 24 for the parse
+      const uint32_t yb = with_bytes ? (w32[ip1 - 1] << 8) & 0xff000000u : (live ? flag : 0u);
+      prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // K5: the lazy parse (deflate_slow) as a per-position state machine over profiles.
+// The parse walks its segment forward, so profiles are fetched PR_CHUNK at a time
+// (32-byte aligned vector loads into registers), with the following chunk
+// already in flight, instead of one dependent 8-byte load per position; lanes
+// are padded to 256 positions, so a chunk never leaves the lane's slice of the
+// profile array.  The byte before each position rides in profile.y bits 24-31
+// (K4 stores it), so emitting a literal needs no load of the input.
+constexpr uint32_t PR_CHUNK = 4;
 struct Parser {
-  const uint8_t* src;
   const uint2* prof;  // lane-relative
   uint64_t n;
   uint32_t p, L, avail, dist;
+  uint32_t cb = 0xffffffffu;  // first position of the cached chunk (~0: none)
+  uint4 a01, a23, b01, b23;   // chunks cb and cb + PR_CHUNK
+
+  __device__ __forceinline__ void fetch(uint32_t q, uint4& x01, uint4& x23) {
+    if (q < n) {
+      const uint4* v = reinterpret_cast<const uint4*>(prof + q);
+      x01 = __ldg(v);
+      x23 = __ldg(v + 1);
+    }
+  }
+  __device__ __forceinline__ uint2 prof_at(uint32_t q) {
+    const uint32_t qb = q & ~(PR_CHUNK - 1);
+    if (qb != cb) {
+      if (qb == cb + PR_CHUNK)
+        a01 = b01, a23 = b23;
+      else
+        fetch(qb, a01, a23);
+      cb = qb;
+      fetch(qb + PR_CHUNK, b01, b23);
+    }
+    const uint32_t k = q - cb;
+    const uint4 h = k & 2 ? a23 : a01;
+    return k & 1 ? make_uint2(h.z, h.w) : make_uint2(h.x, h.y);
+  }
 
   // One loop-top iteration at p < n.  Returns a symbol or 0 (none).
   __device__ __forceinline__ uint32_t step() {
-    uint32_t ml = MIN_MATCH - 1, md = 0;
+    uint32_t ml = MIN_MATCH - 1, md = 0, prev_byte = 0;
     if (L < MAX_LAZY) {
-      uint2 pr = __ldg(&prof[p]);
-      uint32_t v = L >= GOOD_LENGTH ? pr.y : pr.x;
-      bool nil = (v & PROF_AT_MAXDIST) && nil_head_at(p, n);
-      uint32_t len = v & 0x1ff;
+      const uint2 pr = prof_at(p);
+      const uint32_t v = L >= GOOD_LENGTH ? pr.y : pr.x;
+      const bool nil = (pr.x & PROF_AT_MAXDIST) && nil_head_at(p, n);
+      const uint32_t len = v & 0x1ff;
       if (!nil && len > L) ml = len, md = (v >> 9) & 0x7fff;
+      prev_byte = pr.y >> 24;
     }
     if (L >= MIN_MATCH && ml <= L) {
       uint32_t sym = SYM_MATCH | (L - MIN_MATCH) | ((dist - 1) << 8);
@@ -701,8 +738,9 @@ struct Parser {
       dist = 0;
       return sym;
     }
+    // (a literal is only emitted when L < MIN_MATCH, so the profile was read)
     uint32_t sym = 0;
-    if (avail) sym = 0x40000000u | src[p - 1];  // bit 30 marks "literal present"
+    if (avail) sym = 0x40000000u | prev_byte;  // bit 30 marks "literal present"
     avail = 1;
     p++;
     L = ml;
@@ -727,10 +765,21 @@ __global__ void k_parse_spec(const LaneDev* __restrict__ lanes, int nlanes,
   const uint32_t k = g - Ld.seg0;
   const uint64_t s = (uint64_t)k * Ld.G;
   const uint64_t e = umin64(s + Ld.G, Ld.n);
-  Parser P{Ld.src, prof + Ld.pbase, Ld.n, (uint32_t)s, MIN_MATCH - 1, 0, 0};
+  Parser P{prof + Ld.pbase, Ld.n, (uint32_t)s, MIN_MATCH - 1, 0, 0};
   uint32_t* out = spec_syms + (uint64_t)g * sym_stride;
   uint2* sm = state_map + (uint64_t)g * CONV_W;
   uint32_t cnt = 0, next_w = 0;
+  // symbols leave four at a time as one 16-byte store (rows are 16-byte aligned)
+  uint4 buf = make_uint4(0, 0, 0, 0);
+  auto put = [&](uint32_t v) {
+    const uint32_t j = cnt & 3;
+    buf.x = j == 0 ? v : buf.x;
+    buf.y = j == 1 ? v : buf.y;
+    buf.z = j == 2 ? v : buf.z;
+    buf.w = j == 3 ? v : buf.w;
+    if (j == 3) *reinterpret_cast<uint4*>(out + cnt - 3) = buf;
+    cnt++;
+  };
   while (P.p < e) {
     uint32_t rel = P.p - (uint32_t)s;
     if (rel < CONV_W) {
@@ -739,13 +788,19 @@ __global__ void k_parse_spec(const LaneDev* __restrict__ lanes, int nlanes,
       next_w = rel + 1;
     }
     uint32_t sym = P.step();
-    if (sym) out[cnt++] = sym_clean(sym);
+    if (sym) put(sym_clean(sym));
   }
   for (; next_w < CONV_W; next_w++) sm[next_w] = make_uint2(0, 0);
   uint32_t post = 0;
   if (k == Ld.nseg - 1 && P.p >= Ld.n && P.avail) {
-    out[cnt++] = Ld.src[Ld.n - 1];
+    put(Ld.src[Ld.n - 1]);
     post = 1;
+  }
+  {
+    const uint32_t j = cnt & 3, b0 = cnt - j;  // the partial last group
+    if (j > 0) out[b0] = buf.x;
+    if (j > 1) out[b0 + 1] = buf.y;
+    if (j > 2) out[b0 + 2] = buf.z;
   }
   spec_exit[g] = SegExit{P.p, P.state()};
   spec_cnt[g] = cnt;
@@ -780,7 +835,7 @@ __global__ void k_parse_fixup(const LaneDev* __restrict__ lanes, const uint32_t*
   entry_used[g] = entry;
   const uint64_t s = (uint64_t)k * Ld.G;
   const uint64_t e = umin64(s + Ld.G, Ld.n);
-  Parser P{Ld.src, prof + Ld.pbase, Ld.n, entry.p, entry.state & 0x1ff, (entry.state >> 9) & 1,
+  Parser P{prof + Ld.pbase, Ld.n, entry.p, entry.state & 0x1ff, (entry.state >> 9) & 1,
            (entry.state >> 10) & 0x7fff};
   const uint2* sm = state_map + (uint64_t)g * CONV_W;
   uint32_t* out = fix_syms + (uint64_t)g * sym_stride;
@@ -1808,7 +1863,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     blk_total += d.nblk_max;
     maxG = std::max(maxG, d.G);
   }
-  const uint32_t sym_stride = maxG + 1;
+  const uint32_t sym_stride = (maxG + 1 + 3) & ~3u;  // 16-byte aligned segment rows (K5 vector stores)
   std::vector<uint64_t> lane_prefix(nl + 1, 0);
   for (int i = 0; i < nl; i++) lane_prefix[i + 1] = lane_prefix[i] + L[i].n;
   const uint64_t npos_exact = lane_prefix[nl];
@@ -1888,7 +1943,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   }
   T.mark("deflate.profile");
   if (!pf_work.empty()) {
-    k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof);
+    k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof, 1);
     BB_LAUNCH_CHECK();
   }
   // K5: speculative parse, then fix-up rounds until no exit state changes
@@ -2017,7 +2072,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   }
   if (!pf.empty() && d_prof) {
     size_t smem = 4 * PF_WIN;
-    k_profile3<<<(unsigned)pf.size(), PF_THREADS, smem + 16, st>>>(dl, dp, d_pd, reinterpret_cast<uint2*>(d_prof));
+    k_profile3<<<(unsigned)pf.size(), PF_THREADS, smem + 16, st>>>(dl, dp, d_pd, reinterpret_cast<uint2*>(d_prof), 0);
     BB_LAUNCH_CHECK();
   }
   BB_CUDA_TRY(cudaStreamSynchronize(st));

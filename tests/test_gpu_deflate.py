@@ -41,6 +41,15 @@ def _corpus():
     for per in (1, 2, 3, 7, 258, 300):
         pat = rng.randbytes(per)
         yield (pat * (150000 // per + 1))[:150000]
+    # hash heads exactly MAX_DIST (32506) back: zlib compares the head before its
+    # limit test, so these matches must be found (one head per K4 segment phase)
+    # (background from a 4-symbol alphabet, chunk from bytes 128-255: the chunk's
+    # 3-grams have no other occurrence, so the head is exactly the first copy)
+    for at in (100, 16000, 40000):
+        buf = bytearray(rng.choice(b"\x00\x01\x02\x03") for _ in range(at + 32506 + 5000))
+        buf[at:at + 24] = bytes(rng.randrange(128, 256) for _ in range(24))
+        buf[at + 32506:at + 32506 + 24] = buf[at:at + 24]
+        yield bytes(buf)
 
 
 def test_hash_prev_and_profiles_match_oracle(codec, oracle):
