@@ -340,40 +340,52 @@ WORKLOADS = {
 
 
 class Clocks:
-    """nvidia-smi samples during the timed region."""
+    """nvidia-smi samples (every 50 ms) kept for the timed region [t0, t1] (wall clock).
+
+    The sampler is started before the warm-up so that short timed regions are covered; a region
+    shorter than the sampling period reports the nearest sample and says so."""
 
     def __init__(self, dev: int):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap,power.draw")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
 
-    def stop(self) -> dict:
+    def stop(self, t0: float = None, t1: float = None) -> dict:
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        import datetime
         self.p.terminate()
         out, _ = self.p.communicate(timeout=10)
-        sm, mx, reasons = [], [], set()
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[1]), float(f[2]), {nm for nm, v in zip(names, f[4:8]) if v.lower() == "active"}))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        sel, nearest = rows, False
+        if t0 is not None and rows:
+            sel = [r for r in rows if t0 <= r[0] <= t1]
+            if not sel:  # region shorter than the sampling period
+                mid = 0.5 * (t0 + t1)
+                sel, nearest = [min(rows, key=lambda r: abs(r[0] - mid))], True
+        reasons = set().union(*[r[3] for r in sel]) if sel else set()
+        res = {"sm_mhz": statistics.median(r[1] for r in sel) if sel else None,
+               "sm_max_mhz": max(r[2] for r in sel) if sel else None,
+               "samples": 0 if nearest else len(sel), "reasons": sorted(reasons)}
+        if nearest:
+            res["nearest_sample_s"] = round(min(abs(sel[0][0] - t0), abs(sel[0][0] - t1)), 3)
+        return res
 
 
 def dist_init():
@@ -598,6 +610,7 @@ def main():
         return comp
 
     comp_step = 0
+    clocks = Clocks(dev_id)  # started before the warm-up; only timed-region samples are kept
     for _ in range(args.warmup):
         comp_step = step()
     torch.cuda.synchronize()
@@ -607,20 +620,21 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = Clocks(dev_id)
     _lib.stage_timing(True)
     _lib.stage_report(reset=True)
     launches0 = _lib.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
     ev0.record()
     for _ in range(args.steps):
         comp_step = step()
     ev1.record()
     torch.cuda.synchronize()
+    t_wall1 = time.time()
     launches = _lib.kernel_launches() - launches0
     stages = _lib.stage_report(reset=True)
     _lib.stage_timing(False)
-    clk = clocks.stop()
+    clk = clocks.stop(t_wall0, t_wall1)
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
