@@ -713,6 +713,15 @@ def main():
         if limiter:  # the on-chip resource the kernel actually saturates (from the committed ncu capture)
             roof["limiter"] = limiter
     codec_roof = 2 * (raw_step + comp_step) / (ms_step / 1e3) / 1e9
+    # SURVEY 8(d) per-direction figures: (raw + container) / t over the device stage timers of each side
+    per_dir = None
+    if stages:
+        t_enc = sum(v["ms"] for k, v in stages.items() if k.startswith("deflate.")) / args.steps
+        t_dec = sum(v["ms"] for k, v in stages.items() if k.startswith("inflate.")) / args.steps
+        if t_enc > 0 and t_dec > 0:
+            per_dir = {"enc_ms": t_enc, "enc_gbs": (raw_step + comp_step) / (t_enc / 1e3) / 1e9,
+                       "dec_ms": t_dec, "dec_gbs": (raw_step + comp_step) / (t_dec / 1e3) / 1e9,
+                       "source": "sum of the per-stage CUDA-event timers of each direction (per GPU)"}
 
     cpu = None
     bit_exact = None
@@ -759,7 +768,8 @@ def main():
         "pipeline_tokens_per_s": wl.tokens_per_step / (ms_step / 1e3),
         "pipeline_steps_per_s": 1e3 / ms_step,
         "codec_roofline": {"achieved": codec_roof, "peak": hbm, "frac": codec_roof / hbm,
-                           "definition": "2*(raw+container)/(t_enc+t_dec), SURVEY 8(d)"},
+                           "definition": "2*(raw+container)/(t_enc+t_dec), SURVEY 8(d)",
+                           "per_direction": per_dir},
         "roofline": roof, "stages_ms_per_step": {k: v["ms"] / args.steps for k, v in stages.items()},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
     }
