@@ -446,12 +446,14 @@ __global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __r
   const uint64_t B0 = 4 * T;
   const int lane = threadIdx.x & 31;
   uint32_t sbits = 0;
+  uint64_t x0_keep = 0;
   if (find_dynamic) {
     uint32_t cm = 0;
     uint64_t x0 = 0, x1 = 0;
     if (B0 < J.n) {
       const uint64_t nbits = 8 * J.n;
       x0 = peek64(J.src, J.n, 8 * B0), x1 = peek64(J.src, J.n, 8 * B0 + 64);
+      x0_keep = x0;
       uint64_t m = ~(x0 >> 1) & (x0 >> 2);
       m &= ~((x0 >> 4) & (x0 >> 5) & (x0 >> 6) & (x0 >> 7));
       m &= ~((x0 >> 9) & (x0 >> 10) & (x0 >> 11) & (x0 >> 12));
@@ -518,7 +520,17 @@ __global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __r
       }
     }
   }
-  if (B0 < J.n) {
+  if (B0 + 16 <= J.n) {
+    // bytes B0 .. B0 + 7 in one aligned pair of loads: LEN / NLEN at each of the 4 offsets
+    const uint64_t x = find_dynamic ? x0_keep : peek64(J.src, J.n, 8 * B0);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t B = B0 + k;
+      const uint32_t w = (uint32_t)(x >> (8 * k));
+      const uint32_t len = w & 0xffff, nlen = w >> 16;
+      if (B >= 2 && len == (~nlen & 0xffff) && B + 4 + len <= J.n) sbits |= 1u << k;
+    }
+  } else if (B0 < J.n) {
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       const uint64_t B = B0 + k;
