@@ -46,7 +46,10 @@ namespace bb {
 namespace par {
 
 constexpr uint32_t SENT_END = 0xFFFFFFF0u, SENT_BREAK = 0xFFFFFFF1u, SENT_BAD = 0xFFFFFFF2u;
-constexpr int ND_THREADS = 128;
+#ifndef ND_THREADS_OVR
+#define ND_THREADS_OVR 128
+#endif
+constexpr int ND_THREADS = ND_THREADS_OVR;
 constexpr uint32_t SUB = 32768;  // resolution window
 constexpr uint32_t MOD = 65521;
 
@@ -677,7 +680,10 @@ __global__ void __launch_bounds__(ND_THREADS) k_decode_nodes(const PJob* __restr
 // starts, and the true decode entering a chunk (the previous lane's exit) is
 // advanced only until it lands on one of them.  Pass 2 (k_dyn_emit) then
 // decodes every lane's exact sub-range again, writing its output.
-constexpr int WD_WARPS = 2;
+#ifndef WD_WARPS_OVR
+#define WD_WARPS_OVR 2
+#endif
+constexpr int WD_WARPS = WD_WARPS_OVR;
 __device__ unsigned long long g_wd[8];  // watchdog trips per loop site (debug)
 __device__ unsigned* g_prog;             // debug: progress words in mapped host memory (or null)
 #ifdef BB_PROG_DEBUG  // progress words for hang diagnosis (kept out of the hot loops otherwise)
@@ -863,7 +869,10 @@ struct WarpSm {
   uint16_t rnm[32][REC];   // matches before record j
 };
 
-__global__ void __launch_bounds__(32 * WD_WARPS, 5) k_dyn_scan(const PJob* __restrict__ jobs,
+#ifndef DS_MINB
+#define DS_MINB 5
+#endif
+__global__ void __launch_bounds__(32 * WD_WARPS, DS_MINB) k_dyn_scan(const PJob* __restrict__ jobs,
                                                            const uint32_t* __restrict__ node_job,
                                                            const uint32_t* __restrict__ dyn_nodes, uint32_t ndyn_total,
                                                            Node* __restrict__ nodes, Tables* __restrict__ tabs,
@@ -1468,7 +1477,10 @@ __device__ uint64_t first_match_after(const Match* m, uint64_t count, uint64_t x
 }
 
 constexpr uint32_t RESOLVED = 0x80000000u;
-constexpr int RS_THREADS = 1024;
+#ifndef RS_THREADS_OVR
+#define RS_THREADS_OVR 1024
+#endif
+constexpr int RS_THREADS = RS_THREADS_OVR;
 
 struct ExtEntry {
   uint32_t dst;
