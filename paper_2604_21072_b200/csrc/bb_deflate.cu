@@ -220,7 +220,10 @@ __device__ __forceinline__ void hp_load_tile(const uint8_t* src, uint64_t n, uin
 // No history pass: each position is scanned once.  (Measured alternatives --
 // one warp per 1024 positions with a block radix sort, a block-parallel scan with
 // per-hash warp masks, a device-wide key sort -- were slower; see profiles/.)
-constexpr uint32_t HP4_SEG = 32768;
+#ifndef HP4_SEG_OVR
+#define HP4_SEG_OVR 32768
+#endif
+constexpr uint32_t HP4_SEG = HP4_SEG_OVR;
 constexpr int HP6_D = 8;
 
 __device__ __forceinline__ uint32_t hp_hash_at(uint32_t w, uint32_t x, int k, int lane) {
@@ -317,7 +320,10 @@ __global__ void __launch_bounds__(32) k_hash_prev6(const LaneDev* __restrict__ l
 // only the head-table part of each tile (read heads, then store the tile's last
 // occurrences) runs in tile order, handed from warp to warp by named barriers
 // (the finishing warp arrives, the next one syncs).
-constexpr int HP7_W = 4;
+#ifndef HP7_W_OVR
+#define HP7_W_OVR 4
+#endif
+constexpr int HP7_W = HP7_W_OVR;
 
 __global__ void __launch_bounds__(32 * HP7_W) k_hash_prev7(const LaneDev* __restrict__ lanes,
                                                           const WorkItem* __restrict__ work,
