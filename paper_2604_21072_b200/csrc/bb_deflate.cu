@@ -325,10 +325,14 @@ __global__ void __launch_bounds__(32) k_hash_prev6(const LaneDev* __restrict__ l
 #endif
 constexpr int HP7_W = HP7_W_OVR;
 
+#ifndef HP7_TP
+#define HP7_TP 4  // consecutive 128-position tiles per warp turn (one hand-over per turn)
+#endif
 __global__ void __launch_bounds__(32 * HP7_W) k_hash_prev7(const LaneDev* __restrict__ lanes,
                                                           const WorkItem* __restrict__ work,
                                                           uint16_t* __restrict__ pd,
                                                           uint16_t* __restrict__ seg_heads) {
+  constexpr int TP = HP7_TP;
   extern __shared__ uint16_t hp7_head[];  // position - s + 1 (0 = none)
   const WorkItem w = work[blockIdx.x];
   const LaneDev L = lanes[w.lane];
@@ -342,52 +346,73 @@ __global__ void __launch_bounds__(32 * HP7_W) k_hash_prev7(const LaneDev* __rest
   uint16_t* out = pd + L.pbase;
   for (int i = threadIdx.x; i < 32768 * 2 / 16; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
   const uint32_t ntiles = (uint32_t)((e - s + 127) / 128);
-  uint32_t cw = 0, cx = 0;
-  if ((uint32_t)wid < ntiles) hp_load_tile(src, n, s + 128ull * wid, lane, cw, cx);
+  uint32_t cw[TP], cx[TP];
+#pragma unroll
+  for (int u = 0; u < TP; u++) {
+    cw[u] = cx[u] = 0;
+    const uint32_t t = (uint32_t)wid * TP + u;
+    if (t < ntiles) hp_load_tile(src, n, s + 128ull * t, lane, cw[u], cx[u]);
+  }
   __syncthreads();
-  for (uint32_t t = wid; t < ntiles; t += HP7_W) {
-    const uint64_t c = s + 128ull * t;
-    uint32_t nw = 0, nx = 0;
-    if (t + HP7_W < ntiles) hp_load_tile(src, n, c + 128ull * HP7_W, lane, nw, nx);  // this warp's next tile
-    uint32_t h[4];
-    unsigned peers[4];
-    bool valid[4];
+  for (uint32_t t0 = (uint32_t)wid * TP; t0 < ntiles; t0 += HP7_W * TP) {
+    uint32_t nw[TP], nx[TP];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint64_t q = c + 32 * k + lane;
-      valid[k] = q < e && q + MIN_MATCH <= n;
-      const uint32_t hh = hp_hash_at(cw, cx, k, lane);
-      h[k] = valid[k] ? hh : 0x10000u + lane;
+    for (int u = 0; u < TP; u++) {  // this warp's next turn
+      nw[u] = nx[u] = 0;
+      const uint32_t t = t0 + HP7_W * TP + u;
+      if (t < ntiles) hp_load_tile(src, n, s + 128ull * t, lane, nw[u], nx[u]);
     }
+    uint32_t h[TP][4];
+    unsigned peers[TP][4];
+    bool valid[TP][4];
 #pragma unroll
-    for (int k = 0; k < 4; k++) peers[k] = __match_any_sync(0xffffffffu, h[k]);
-    // wait for tile t - 1's head updates (named barrier: its warp arrives, this one syncs)
-    if (t > 0) asm volatile("bar.sync %0, 64;" ::"r"(1 + (wid + HP7_W - 1) % HP7_W) : "memory");
-    uint32_t d[4];
+    for (int u = 0; u < TP; u++) {
+      const uint64_t c = s + 128ull * (t0 + u);
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint64_t q = c + 32 * k + lane;
-      const unsigned lower = peers[k] & ((1u << lane) - 1);
-      d[k] = 0;
-      if (valid[k]) {
-        if (lower) {
-          d[k] = lane - (31 - __clz(lower));
-        } else {
-          const uint32_t r = head[h[k]];
-          d[k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
-        }
+      for (int k = 0; k < 4; k++) {
+        const uint64_t q = c + 32 * k + lane;
+        valid[u][k] = q < e && q + MIN_MATCH <= n;
+        const uint32_t hh = hp_hash_at(cw[u], cx[u], k, lane);
+        h[u][k] = valid[u][k] ? hh : 0x10000u + lane;
       }
-      __syncwarp();
-      if (valid[k] && (peers[k] >> lane) == 1u) head[h[k]] = (uint16_t)(q - s + 1);
-      __syncwarp();
-    }
-    if (t + 1 < ntiles) asm volatile("bar.arrive %0, 64;" ::"r"(1 + wid) : "memory");
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const uint64_t q = c + 32 * k + lane;
-      if (q < e) out[q] = (uint16_t)d[k];
+      for (int k = 0; k < 4; k++) peers[u][k] = __match_any_sync(0xffffffffu, h[u][k]);
     }
-    cw = nw, cx = nx;
+    // wait for the previous turn's head updates (named barrier: its warp arrives, this one syncs)
+    if (t0 > 0) asm volatile("bar.sync %0, 64;" ::"r"(1 + (wid + HP7_W - 1) % HP7_W) : "memory");
+    uint32_t d[TP][4];
+#pragma unroll
+    for (int u = 0; u < TP; u++) {
+      const uint64_t c = s + 128ull * (t0 + u);
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint64_t q = c + 32 * k + lane;
+        const unsigned lower = peers[u][k] & ((1u << lane) - 1);
+        d[u][k] = 0;
+        if (valid[u][k]) {
+          if (lower) {
+            d[u][k] = lane - (31 - __clz(lower));
+          } else {
+            const uint32_t r = head[h[u][k]];
+            d[u][k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
+          }
+        }
+        __syncwarp();
+        if (valid[u][k] && (peers[u][k] >> lane) == 1u) head[h[u][k]] = (uint16_t)(q - s + 1);
+        __syncwarp();
+      }
+    }
+    if (t0 + TP < ntiles) asm volatile("bar.arrive %0, 64;" ::"r"(1 + wid) : "memory");
+#pragma unroll
+    for (int u = 0; u < TP; u++) {
+      const uint64_t c = s + 128ull * (t0 + u);
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint64_t q = c + 32 * k + lane;
+        if (q < e) out[q] = (uint16_t)d[u][k];
+      }
+      cw[u] = nw[u], cx[u] = nx[u];
+    }
   }
   __syncthreads();
   uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)blockIdx.x * 32768);
