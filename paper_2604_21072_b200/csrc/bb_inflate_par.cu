@@ -1719,7 +1719,10 @@ __global__ void __cluster_dims__(RS_CL, 1, 1) __launch_bounds__(RS_THREADS)
 // Every byte left unresolved by its window points to an earlier byte; chase
 // the pointers (read-only map) to a byte its own window resolved.  Fully
 // parallel over all windows of all lanes.
-__global__ void __launch_bounds__(256) k_resolve_chase(const PJob* __restrict__ jobs,
+#ifndef RC_THREADS
+#define RC_THREADS 1024
+#endif
+__global__ void __launch_bounds__(RC_THREADS) k_resolve_chase(const PJob* __restrict__ jobs,
                                                       const uint32_t* __restrict__ job_of_sub,
                                                       uint32_t* __restrict__ fail,
                                                       const ExtEntry* __restrict__ ext,
@@ -1951,7 +1954,13 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   BB_LAUNCH_CHECK();
   if (find_dynamic) {
     T.mark("inflate.verify_headers");
-    k_verify_dynamic<<<kNumSMs * 8, 128, 0, st>>>(d_jobs, d_surv, d_surv_cnt, surv_cap, d_dbm, d_fail, nj);
+#ifndef VD_GRID_MUL
+#define VD_GRID_MUL 8
+#endif
+#ifndef VD_THREADS
+#define VD_THREADS 256
+#endif
+    k_verify_dynamic<<<kNumSMs * VD_GRID_MUL, VD_THREADS, 0, st>>>(d_jobs, d_surv, d_surv_cnt, surv_cap, d_dbm, d_fail, nj);
     BB_LAUNCH_CHECK();
   }
   T.mark("inflate.rank_scan");
@@ -2143,7 +2152,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
           d_jobs, d_clm, d_out_total, d_fail, d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
     }
     BB_LAUNCH_CHECK();
-    k_resolve_chase<<<(unsigned)sub_job.size(), 256, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
+    k_resolve_chase<<<(unsigned)sub_job.size(), RC_THREADS, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
                                                              d_wflag);
     BB_LAUNCH_CHECK();
   }
