@@ -1590,7 +1590,19 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const LaneDev* __restrict__
     // output byte range [byte, byte + 4 + len): word-granular writes
     uint64_t b0 = byte, b1 = byte + 4 + len;
     uint64_t w0 = b0 >> 2, w1 = (b1 + 3) >> 2;
+    const uintptr_t src_end = reinterpret_cast<uintptr_t>(src) + len;
     for (uint64_t wi = w0 + threadIdx.x; wi < w1; wi += blockDim.x) {
+      // interior words: four input bytes from two aligned loads and a funnel shift
+      if (4 * wi >= b0 + 4 && 4 * wi + 4 <= b1) {
+        const uintptr_t ua = reinterpret_cast<uintptr_t>(src) + (4 * wi - b0 - 4);
+        const uintptr_t base = ua & ~uintptr_t(3);
+        if (base + 8 <= src_end) {
+          const uint32_t lo = __ldg(reinterpret_cast<const uint32_t*>(base));
+          const uint32_t hi = __ldg(reinterpret_cast<const uint32_t*>(base) + 1);
+          reinterpret_cast<uint32_t*>(ob)[wi] = __funnelshift_r(lo, hi, 8 * (uint32_t)(ua & 3));
+          continue;
+        }
+      }
       uint32_t v = 0, mask = 0;
       for (int k = 0; k < 4; k++) {
         uint64_t ob_i = 4 * wi + k;
