@@ -501,11 +501,18 @@ __global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __r
       if (k < tot) {
         const uint32_t slot = k - (oinc - ocnt);
         i = __fns(ocm, 0, (int)slot + 1);
-        const uint32_t ncode = bits_at(wx0, wx1, i + 13, 4) + 4;
+        // HCLEN and the 19 code-length-code lengths: 61 bits from offset i + 13 (<= 44)
+        const uint32_t sh = i + 13;
+        const uint64_t y = (wx0 >> sh) | (wx1 << (64 - sh));
+        const uint32_t ncode = (uint32_t)(y & 15) + 4;
+        // Kraft sum of the first ncode 3-bit lengths, 128 >> l from a byte table
+        // (0, 64, 32, 16, 8, 4, 2, 1); complete iff the sum is exactly 128
         uint32_t kraft = 0;
-        for (uint32_t kk = 0; kk < ncode && kraft <= 128; kk++) {
-          const uint32_t l = bits_at(wx0, wx1, i + 17 + 3 * kk, 3);
-          kraft += l ? (128u >> l) : 0u;
+#pragma unroll
+        for (uint32_t kk = 0; kk < 19; kk++) {
+          const uint32_t l = (uint32_t)(y >> (4 + 3 * kk)) & 7;
+          const uint32_t v = __byte_perm(0x10204000u, 0x01020408u, l);
+          kraft += kk < ncode ? v : 0u;
         }
         pass = kraft == 128;
       }
