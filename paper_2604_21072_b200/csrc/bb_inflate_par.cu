@@ -410,27 +410,6 @@ __device__ bool verify_dynamic(const uint8_t* p, uint64_t n, uint64_t b) {
 }
 
 // ---- P1 --------------------------------------------------------------------
-__device__ __forceinline__ uint32_t bits_at(uint64_t w0, uint64_t w1, uint32_t off, uint32_t k) {
-  uint64_t v = off < 64 ? (w0 >> off) | (off ? (w1 << (64 - off)) : 0) : (w1 >> (off - 64));
-  return (uint32_t)(v & ((1ull << k) - 1));
-}
-
-// Necessary conditions for a dynamic header at bit `k` of the 128-bit window
-// (w0, w1): BTYPE = 10, HLIT <= 29, HDIST <= 29 and a complete code-length code.
-__device__ __forceinline__ bool dyn_header_quick(uint64_t w0, uint64_t w1, uint32_t k) {
-  const uint64_t x0 = k ? (w0 >> k) | (w1 << (64 - k)) : w0;
-  const uint64_t x1 = w1 >> k;
-  if (((x0 >> 1) & 3) != 2) return false;
-  if (((x0 >> 3) & 31) > 29 || ((x0 >> 8) & 31) > 29) return false;
-  const uint32_t ncode = (uint32_t)((x0 >> 13) & 15) + 4;
-  uint32_t kraft = 0;
-#pragma unroll
-  for (uint32_t i = 0; i < 19; i++) {
-    const uint32_t l = bits_at(x0, x1, 17 + 3 * i, 3);
-    kraft += (i < ncode && l) ? (128u >> l) : 0u;
-  }
-  return kraft == 128;
-}
 
 // Survivors of the quick test are appended to a list (warp-aggregated) and
 // verified exactly by k_verify_dynamic with one thread each, so the rare long
@@ -780,6 +759,7 @@ struct WordReader {
   uint64_t hold;
   int bits;
   uint32_t used;  // bits consumed since init
+  uint32_t nxt;   // word wi, loaded one refill ahead (its latency hides behind ~32 bits of decode)
   __device__ __forceinline__ uint32_t word(uint32_t k) const { return k < wend ? __ldg(w + k) : 0u; }
   __device__ __forceinline__ void init(const uint8_t* p, uint64_t n, uint64_t bitpos) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(p);
@@ -790,12 +770,14 @@ struct WordReader {
     hold = ((uint64_t)word(k) | ((uint64_t)word(k + 1) << 32)) >> sh;
     bits = 64 - (int)sh;
     wi = k + 2;
+    nxt = word(wi);
     used = 0;
   }
   __device__ __forceinline__ void refill() {
     if (bits <= 32) {
-      hold |= (uint64_t)word(wi++) << bits;
+      hold |= (uint64_t)nxt << bits;
       bits += 32;
+      nxt = word(++wi);
     }
   }
   __device__ __forceinline__ void drop(uint32_t k) {
