@@ -556,6 +556,14 @@ __global__ void k_verify_dynamic(const PJob* __restrict__ jobs, const uint64_t* 
   }
 }
 
+// node-count prefix values for the host: entries 4i, 4i + 1 index the dynamic
+// prefix array, 4i + 2, 4i + 3 the stored one
+__global__ void k_gather_prefix(const uint64_t* __restrict__ idx, int n, const uint32_t* __restrict__ dpre,
+                                const uint32_t* __restrict__ spre, uint32_t* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = ((k & 3) < 2 ? dpre : spre)[idx[k]];
+}
+
 __global__ void k_popc(const uint32_t* __restrict__ words, uint64_t count, uint32_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = __popc(words[i]);
@@ -1832,9 +1840,12 @@ struct ParInflate {
   size_t h_cap = 0;
   void* scan_tmp = nullptr;
   size_t scan_cap = 0;
+  uint64_t* cnt_idx = nullptr;  // device: 4 prefix indices per job (node counts), then the gathered values
+  size_t cnt_cap = 0;
   ~ParInflate() {
     if (h_pin) cudaFreeHost(h_pin);
     if (scan_tmp) cudaFree(scan_tmp);
+    if (cnt_idx) cudaFree(cnt_idx);
   }
 };
 
@@ -1977,15 +1988,26 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     BB_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P->h_pin), 16 * nj + 64, cudaHostAllocDefault));
     P->h_cap = 4 * nj + 8;
   }
-  std::vector<uint64_t> need_idx;
-  for (int i = 0; i < nj; i++) {
-    // count = prefix[next job's first word] - prefix[first word]; last words are padding (zero)
-    uint64_t dend = J[i].dbm + (J[i].n + 3) / 4;
-    uint64_t send = J[i].sbm + (J[i].n + 31) / 32 + 1;
-    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i, d_dpre + J[i].dbm, 4, cudaMemcpyDeviceToHost, st));
-    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i + 1, d_dpre + dend, 4, cudaMemcpyDeviceToHost, st));
-    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i + 2, d_spre + J[i].sbm, 4, cudaMemcpyDeviceToHost, st));
-    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin + 4 * i + 3, d_spre + send, 4, cudaMemcpyDeviceToHost, st));
+  {
+    // count = prefix[next job's first word] - prefix[first word]; last words are padding (zero).
+    // The 4 nj prefix values are gathered on the device and come back in one copy.
+    std::vector<uint64_t> idx(4 * nj);
+    for (int i = 0; i < nj; i++) {
+      idx[4 * i] = J[i].dbm;
+      idx[4 * i + 1] = J[i].dbm + (J[i].n + 3) / 4;
+      idx[4 * i + 2] = J[i].sbm;
+      idx[4 * i + 3] = J[i].sbm + (J[i].n + 31) / 32 + 1;
+    }
+    if ((size_t)(8 * nj) > P->cnt_cap) {
+      if (P->cnt_idx) cudaFree(P->cnt_idx);
+      BB_CUDA_TRY(cudaMalloc(&P->cnt_idx, 8 * 8 * (size_t)nj));
+      P->cnt_cap = 8 * nj;
+    }
+    uint32_t* d_cnt = reinterpret_cast<uint32_t*>(P->cnt_idx + 4 * nj);
+    BB_CUDA_TRY(cudaMemcpyAsync(P->cnt_idx, idx.data(), 8 * idx.size(), cudaMemcpyHostToDevice, st));
+    k_gather_prefix<<<(4 * nj + 127) / 128, 128, 0, st>>>(P->cnt_idx, 4 * nj, d_dpre, d_spre, d_cnt);
+    BB_LAUNCH_CHECK();
+    BB_CUDA_TRY(cudaMemcpyAsync(P->h_pin, d_cnt, 16 * (size_t)nj, cudaMemcpyDeviceToHost, st));
   }
   BB_CUDA_TRY(cudaStreamSynchronize(st));
   uint32_t nnodes = 0, ndyn_total = 0;
@@ -2075,7 +2097,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   k_chain_len<<<(nj + 63) / 64, 64, 0, st>>>(d_jobs, nj, d_jump, nnodes, levels, d_chains);
   BB_LAUNCH_CHECK();
   {
-    dim3 g(std::max<unsigned>(1, std::min<unsigned>((nnodes + 255) / 256, 4096)), nj);
+    dim3 g(std::max<unsigned>(1, std::min<unsigned>((nnodes + 255) / 256, 64)), nj);  // grid-stride over each chain
     k_chain_nodes<<<g, 256, 0, st>>>(d_jobs, d_chains, d_jump, nnodes, levels, d_chain_nodes);
     BB_LAUNCH_CHECK();
   }
