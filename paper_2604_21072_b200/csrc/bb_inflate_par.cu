@@ -556,6 +556,48 @@ __global__ void k_verify_dynamic(const PJob* __restrict__ jobs, const uint64_t* 
   }
 }
 
+// Stored-only pass (the incompressible lanes): 16 byte offsets per thread from
+// six aligned word loads, realigned once with funnel shifts; same blocks (1 KiB
+// of stream each) and the same stored bitmap as k_candidates4.
+__global__ void __launch_bounds__(64) k_stored_cand(const PJob* __restrict__ jobs,
+                                                   const uint64_t* __restrict__ blk_prefix, int njobs,
+                                                   uint32_t* __restrict__ sbm) {
+  const uint32_t j = (uint32_t)find_job(blk_prefix, njobs, blockIdx.x);
+  const PJob J = jobs[j];
+  const uint64_t T = (blockIdx.x - blk_prefix[j]) * 64ull + threadIdx.x;
+  const uint64_t B0 = 16 * T;  // bytes [B0, B0 + 16)
+  uint32_t bits = 0;
+  if (B0 + 24 <= J.n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(J.src + B0);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = 8 * (uint32_t)(a & 3);
+    uint32_t x[6], y[5];
+#pragma unroll
+    for (int i = 0; i < 6; i++) x[i] = __ldg(w + i);
+#pragma unroll
+    for (int i = 0; i < 5; i++) y[i] = __funnelshift_r(x[i], x[i + 1], sh);  // bytes B0 + 4i ..
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const uint32_t v = __funnelshift_r(y[k >> 2], y[(k >> 2) + 1], 8 * (k & 3));
+      const uint64_t B = B0 + k;
+      const uint32_t len = v & 0xffff, nlen = v >> 16;
+      if (B >= 2 && len == (~nlen & 0xffff) && B + 4 + len <= J.n) bits |= 1u << k;
+    }
+  } else if (B0 < J.n) {
+    for (int k = 0; k < 16; k++) {
+      const uint64_t B = B0 + k;
+      if (B >= 2 && B + 4 <= J.n) {
+        const uint32_t len = __ldg(J.src + B) | ((uint32_t)__ldg(J.src + B + 1) << 8);
+        const uint32_t nlen = __ldg(J.src + B + 2) | ((uint32_t)__ldg(J.src + B + 3) << 8);
+        if (len == (~nlen & 0xffff) && B + 4 + len <= J.n) bits |= 1u << k;
+      }
+    }
+  }
+  uint32_t wv = bits << (16 * (threadIdx.x & 1));
+  wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+  if ((threadIdx.x & 1) == 0 && B0 < J.n + 32) sbm[J.sbm + (B0 >> 5)] = wv;
+}
+
 // node-count prefix values for the host: entries 4i, 4i + 1 index the dynamic
 // prefix array, 4i + 2, 4i + 3 the stored one
 __global__ void k_gather_prefix(const uint64_t* __restrict__ idx, int n, const uint32_t* __restrict__ dpre,
@@ -1949,8 +1991,11 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   // P1
   BB_CUDA_TRY(cudaMemsetAsync(d_surv_cnt, 0, 8, st));
   T.mark(find_dynamic ? "inflate.candidates_dyn" : "inflate.candidates_stored");
-  k_candidates4<<<(unsigned)cand_blocks, 256, 0, st>>>(d_jobs, d_blk_prefix, nj, d_sbm, find_dynamic, d_surv,
-                                                       d_surv_cnt, surv_cap);
+  if (find_dynamic)
+    k_candidates4<<<(unsigned)cand_blocks, 256, 0, st>>>(d_jobs, d_blk_prefix, nj, d_sbm, find_dynamic, d_surv,
+                                                         d_surv_cnt, surv_cap);
+  else
+    k_stored_cand<<<(unsigned)cand_blocks, 64, 0, st>>>(d_jobs, d_blk_prefix, nj, d_sbm);
   BB_LAUNCH_CHECK();
   if (find_dynamic) {
     T.mark("inflate.verify_headers");
