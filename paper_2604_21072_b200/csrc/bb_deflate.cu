@@ -1737,12 +1737,11 @@ __global__ void __launch_bounds__(AD_THREADS) k_adler_chunks(const LaneDev* __re
       for (; i < AD_BYTES; i += 16) {
         uint32_t v[4];
         gather16(p + i, v);
-#pragma unroll
-        for (int k = 0; k < 16; k++) {
-          uint32_t x = (v[k >> 2] >> (8 * (k & 3))) & 0xff;
-          A += x;
-          B += (uint32_t)(m - (i + k)) * x;
-        }
+        // sum x_k and sum k x_k over the 16 bytes: B += sum (m - i - k) x_k
+        const uint32_t sx = __dp4a(v[0], 0x01010101u, __dp4a(v[1], 0x01010101u, __dp4a(v[2], 0x01010101u, __dp4a(v[3], 0x01010101u, 0u))));
+        const uint32_t kx = __dp4a(v[0], 0x03020100u, __dp4a(v[1], 0x07060504u, __dp4a(v[2], 0x0b0a0908u, __dp4a(v[3], 0x0f0e0d0cu, 0u))));
+        A += sx;
+        B += (uint64_t)(m - i) * sx - kx;
       }
     } else {
       for (; i < m; i++) {

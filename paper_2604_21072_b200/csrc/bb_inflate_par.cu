@@ -1812,11 +1812,11 @@ __global__ void __launch_bounds__(PA_THREADS) k_adler_part(const PJob* __restric
   for (; i + 16 <= c1; i += 16) {
     uint32_t v[4];
     gather16(J.dst + i, v);
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      A += (v[k >> 2] >> (8 * (k & 3))) & 0xff;
-      B += A;
-    }
+    // 16 sequential (A += b, B += A) steps: A' = A + sum b, B' = B + 16 A + sum (16 - k) b_k
+    const uint32_t sb = __dp4a(v[0], 0x01010101u, __dp4a(v[1], 0x01010101u, __dp4a(v[2], 0x01010101u, __dp4a(v[3], 0x01010101u, 0u))));
+    const uint32_t wb = __dp4a(v[0], 0x0d0e0f10u, __dp4a(v[1], 0x090a0b0cu, __dp4a(v[2], 0x05060708u, __dp4a(v[3], 0x01020304u, 0u))));
+    B += 16 * A + wb;
+    A += sb;
   }
   for (; i < c1; i++) {
     A += J.dst[i];
