@@ -340,7 +340,8 @@ WORKLOADS = {
 
 
 class Clocks:
-    """nvidia-smi samples (every 50 ms) kept for the timed region [t0, t1] (wall clock).
+    """nvidia-smi samples (every 200 ms: faster polling contends with the driver) kept for the timed
+    region [t0, t1] (wall clock).
 
     The sampler is started before the warm-up so that short timed regions are covered; a region
     shorter than the sampling period reports the nearest sample and says so."""
@@ -351,7 +352,7 @@ class Clocks:
              "clocks_event_reasons.sw_power_cap,power.draw")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
