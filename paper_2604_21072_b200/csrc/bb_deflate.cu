@@ -532,12 +532,21 @@ constexpr uint32_t PF_WIN = WSIZE + PF_SEG + MAX_MATCH + 32;
 // lags by at most one batch during the walk: a candidate that fails the quick
 // reject against the lagging best mismatches at or before it and cannot beat
 // the final best either, so the result is exactly zlib's first maximum.
+// c[t] for a run-time t: a binary select tree on the bits of t (B - 1 selects and
+// log2 B bit tests instead of a compare per element)
 template <int B>
 __device__ __forceinline__ uint32_t pf_pick(const uint32_t (&c)[B], int t) {
-  uint32_t v = c[0];
+  static_assert((B & (B - 1)) == 0, "power-of-two batch");
+  uint32_t l[B];
 #pragma unroll
-  for (int k = 1; k < B; k++) v = t == k ? c[k] : v;
-  return v;
+  for (int k = 0; k < B; k++) l[k] = c[k];
+#pragma unroll
+  for (int w = 1; w < B; w <<= 1) {
+    const bool bit = (t & w) != 0;
+#pragma unroll
+    for (int k = 0; k + w < B; k += 2 * w) l[k] = bit ? l[k + w] : l[k];
+  }
+  return l[0];
 }
 
 constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;
