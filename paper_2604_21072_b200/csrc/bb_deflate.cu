@@ -551,7 +551,7 @@ __device__ __forceinline__ uint32_t pf_pick(const uint32_t (&c)[B], int t) {
 
 constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;
 #ifndef PF_B1
-#define PF_B1 4  // chain steps per batch within the first 32 (budget-32 snapshot)
+#define PF_B1 8  // chain steps per batch within the first 32 (budget-32 snapshot)
 #endif
 #ifndef PF_B2
 #define PF_B2 16  // chain steps per batch for candidates 33..128
