@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     // zlib tests the limit only from the second candidate on (do ... while (prev > limit)):
     // a head exactly at MAX_DIST is still compared, and every later candidate is below it
     const uint32_t lim4 = 4 * lim1 - (live && c0 == lim1 ? 4u : 0u);
+    const uint32_t qw2 = p < e ? w32[ip1 + 2] : 0u;  // bytes p + 2, p + 3 (wlen covers e + 274)
     // one batch of B chain steps, then the recorded candidates in chain order
     auto batch = [&](auto bsize) {
       constexpr int B = decltype(bsize)::value;
@@ -682,14 +683,21 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
           // re-test only if best grew in this flush (else it is the test the step already made)
           if (improved && (((w32[c] ^ wp) | (w32[c + best - 1] ^ w32[ip1 + best - 1])) & 0xffff0000u) != 0)
             continue;
+          // bytes 2, 3 against the position's own pair held in a register (most matches end there)
           uint32_t len = 2;
-          while (len < maxl) {
-            const uint32_t x = (w32[c + len] ^ w32[ip1 + len]) >> 16;
-            if (x) {
-              len += (x & 0xff) == 0;
-              break;
+          const uint32_t x2 = (w32[c + 2] ^ qw2) >> 16;
+          if (x2) {
+            len += (x2 & 0xff) == 0;
+          } else {
+            len = 4;
+            while (len < maxl) {
+              const uint32_t x = (w32[c + len] ^ w32[ip1 + len]) >> 16;
+              if (x) {
+                len += (x & 0xff) == 0;
+                break;
+              }
+              len += 2;
             }
-            len += 2;
           }
           len = min(len, maxl);
           if (len > best) {
