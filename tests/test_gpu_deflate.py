@@ -215,3 +215,52 @@ def test_parallel_inflate_rejects_corruption(codec, oracle):
         except codec.CorruptContainer:
             got_ok = False
         assert got_ok == want_ok
+
+
+def _structured(rng, n):
+    """Random mixture of the structures the level-6 rules branch on: small and large
+    alphabets, runs, copies at distances around MAX_DIST (32506) and WSIZE, copies
+    longer than MAX_MATCH (258) and nice_length (128), near-matches that differ in one
+    byte (first-maximum ties), and text from this repo's own sources."""
+    import glob
+    import os
+    text = b"".join(open(f, "rb").read() for f in sorted(glob.glob(
+        os.path.join(os.path.dirname(__file__), "*.py"))))
+    out = bytearray()
+    while len(out) < n:
+        kind = rng.randrange(7)
+        m = rng.randrange(1, 3000)
+        if kind == 0:
+            out += rng.randbytes(m)
+        elif kind == 1:
+            k = rng.choice((2, 3, 4, 16))
+            out += bytes(rng.randrange(k) for _ in range(m))
+        elif kind == 2:
+            out += bytes([rng.randrange(256)]) * m
+        elif kind in (3, 4) and out:
+            d = rng.choice((1, 2, 3, 257, 258, 259, 4096, 32505, 32506, 32507, 32768,
+                            rng.randrange(1, 40000)))
+            d = min(d, len(out))
+            ln = rng.choice((3, 4, 127, 128, 129, 258, 259, 600, m))
+            src = len(out) - d
+            for i in range(ln):
+                out.append(out[src + i])
+            if kind == 4 and ln > 4:
+                out[-rng.randrange(1, ln)] ^= 1 << rng.randrange(8)
+        else:
+            s = rng.randrange(max(1, len(text) - m))
+            out += text[s:s + m]
+    return bytes(out[:n])
+
+
+def test_lane_encode_structured_fuzz(codec):
+    enc = codec.backend_by_id(codec.kBackendDeflate).encode
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    rng = random.Random(2604)
+    for trial in range(40):
+        n = rng.choice((rng.randrange(1, 5000), rng.randrange(5000, 80000), rng.randrange(80000, 400000)))
+        data = _structured(rng, n)
+        got = enc(data)
+        want = zlib.compress(data, 6)
+        assert got == want, (trial, n, len(got), len(want))
+        assert dec(got, n) == data, (trial, n)
