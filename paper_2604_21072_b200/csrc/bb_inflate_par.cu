@@ -1755,6 +1755,76 @@ __global__ void __cluster_dims__(RS_CL, 1, 1) __launch_bounds__(RS_THREADS)
   cl.sync();  // no CTA may exit while a neighbour can still read its shared memory
 }
 
+// Pointer doubling over the unresolved bytes' source map before the chase: one
+// round moves every pending pointer to its source's pointer, so after R rounds a
+// chain of h hops has ~h / 2^R left.  Chains are long where a lane repeats a
+// short period for many windows (the f32 token-tree planes of config3: every
+// hop of the chase would be one dependent global load, one window back).
+// Entries are read and written concurrently across CTAs; as in the cluster
+// pass, a reader sees an older or a newer pointer of the same chain, and both
+// lead to the same root.
+#ifndef RJ_ROUNDS
+#define RJ_ROUNDS 4  // cap on the rounds (the sampled mean chain length decides how many run)
+#endif
+constexpr int RJ_MAX = 16;
+constexpr uint32_t RJ_SAMPLE = 256;  // one sampled chain per 256 unresolved bytes
+// The rounds pay off only where chains are long, and each costs a pass over all
+// unresolved bytes, so their number is decided on the device from a sampled
+// chase: jstat[0] = hops, jstat[1] = chains sampled; round r runs while the mean
+// chain is longer than 4 << r hops (the bf16 activations of config2 average a few
+// hops and skip the rounds; the f32 token-tree planes of config3 run them).
+__global__ void __launch_bounds__(32) k_resolve_sample(const PJob* __restrict__ jobs,
+                                                      const uint32_t* __restrict__ job_of_sub,
+                                                      const uint32_t* __restrict__ fail,
+                                                      const ExtEntry* __restrict__ ext,
+                                                      const uint32_t* __restrict__ ext_cnt,
+                                                      const uint32_t* __restrict__ extp,
+                                                      const uint8_t* __restrict__ wflag, unsigned long long* jstat) {
+  const uint32_t j = job_of_sub[blockIdx.x];
+  const PJob J = jobs[j];
+  const uint32_t c = fail[j] ? 0u : ext_cnt[blockIdx.x];
+  const ExtEntry* E = ext + (uint64_t)blockIdx.x * SUB;
+  const uint32_t* X = extp + J.xbase;
+  const uint8_t* WF = wflag + J.sub0;
+  uint32_t hops = 0, n = 0;
+  for (uint32_t k = threadIdx.x * RJ_SAMPLE; k < c; k += 32 * RJ_SAMPLE) {
+    uint32_t v = E[k].src, w, h = 1;
+    while (h < 4096 && WF[v / SUB] && (w = X[v]) != 0xFFFFFFFFu && w < v) v = w, h++;
+    hops += h;
+    n++;
+  }
+  hops = __reduce_add_sync(0xffffffffu, hops);
+  n = __reduce_add_sync(0xffffffffu, n);
+  if (threadIdx.x == 0 && n) {
+    atomicAdd(jstat, (unsigned long long)hops);
+    atomicAdd(jstat + 1, (unsigned long long)n);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_resolve_jump(const PJob* __restrict__ jobs,
+                                                       const uint32_t* __restrict__ job_of_sub,
+                                                       const uint32_t* __restrict__ fail,
+                                                       const ExtEntry* __restrict__ ext,
+                                                       const uint32_t* __restrict__ ext_cnt, uint32_t* extp,
+                                                       const uint8_t* __restrict__ wflag,
+                                                       const unsigned long long* __restrict__ jstat, int r) {
+  if (jstat[0] <= jstat[1] * (4ull << r)) return;
+  const uint32_t j = job_of_sub[blockIdx.x];
+  const PJob J = jobs[j];
+  if (fail[j]) return;
+  const uint32_t c = ext_cnt[blockIdx.x];
+  const ExtEntry* E = ext + (uint64_t)blockIdx.x * SUB;
+  uint32_t* X = extp + J.xbase;
+  const uint8_t* WF = wflag + J.sub0;
+  for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
+    const uint32_t d = E[k].dst;
+    const uint32_t v = *(volatile uint32_t*)(X + d);
+    if (v >= d || !WF[v / SUB]) continue;  // corrupt (left to the chase) or resolved root
+    const uint32_t w = *(volatile uint32_t*)(X + v);
+    if (w != 0xFFFFFFFFu && w < v) X[d] = w;
+  }
+}
+
 // Every byte left unresolved by its window points to an earlier byte; chase
 // the pointers (read-only map) to a byte its own window resolved.  Fully
 // parallel over all windows of all lanes.
@@ -1966,6 +2036,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   uint32_t* d_extp = W.take<uint32_t>(xtot + 1);
   uint8_t* d_wflag = W.take<uint8_t>(subs + 1);
   uint2* d_clm = W.take<uint2>(subs + nj + 1);  // (job, first window) per resolution cluster
+  unsigned long long* d_jstat = W.take<unsigned long long>(2);
   const uint64_t surv_cap = find_dynamic ? ntot_bytes / 2 + 4096 : 1;
   uint64_t* d_surv = W.take<uint64_t>(surv_cap);
   unsigned long long* d_surv_cnt = W.take<unsigned long long>(1);
@@ -2208,6 +2279,25 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
           d_jobs, d_clm, d_out_total, d_fail, d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
     }
     BB_LAUNCH_CHECK();
+    static const int jumps = std::min(RJ_MAX, getenv("BB_RESOLVE_JUMPS") ? atoi(getenv("BB_RESOLVE_JUMPS")) : RJ_ROUNDS);
+    if (jumps > 0) {
+      BB_CUDA_TRY(cudaMemsetAsync(d_jstat, 0, sizeof(unsigned long long) * 2, st));
+      k_resolve_sample<<<(unsigned)sub_job.size(), 32, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
+                                                                d_wflag, d_jstat);
+      BB_LAUNCH_CHECK();
+    }
+    for (int r = 0; r < jumps; r++) {
+      k_resolve_jump<<<(unsigned)sub_job.size(), 1024, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
+                                                                 d_wflag, d_jstat, r);
+      BB_LAUNCH_CHECK();
+    }
+    static const bool jdbg = getenv("BB_RESOLVE_DEBUG") != nullptr;
+    if (jumps > 0 && jdbg) {
+      unsigned long long h[2];
+      BB_CUDA_TRY(cudaMemcpyAsync(h, d_jstat, sizeof(h), cudaMemcpyDeviceToHost, st));
+      BB_CUDA_TRY(cudaStreamSynchronize(st));
+      fprintf(stderr, "resolve: sampled %llu chains, mean %.1f hops\n", h[1], h[1] ? (double)h[0] / h[1] : 0.0);
+    }
     k_resolve_chase<<<(unsigned)sub_job.size(), RC_THREADS, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
                                                              d_wflag);
     BB_LAUNCH_CHECK();

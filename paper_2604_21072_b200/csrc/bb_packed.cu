@@ -79,6 +79,19 @@ int bb_pack_sd(const float* d_rows, size_t n_rows, size_t hidden_dim, const uint
     if (h_request_rows[r + 1] < h_request_rows[r] || h_request_rows[r + 1] > n_rows)
       return fail(BB_INVALID_ARG, "pack_sd: request row ranges must be ordered and in range");
   if (h_request_rows[0] != 0) return fail(BB_INVALID_ARG, "pack_sd: request rows must start at 0");
+  // the scratch below comes from the device's stream-ordered pool: keep freed
+  // blocks in the pool (the default threshold 0 unmaps them at every synchronize,
+  // so each call would map them again through the driver)
+  static thread_local int pool_dev = -1;
+  int dev = 0;
+  BB_CUDA_TRY(cudaGetDevice(&dev));
+  if (pool_dev != dev) {
+    cudaMemPool_t pool;
+    BB_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep_bytes = 64ull << 20;
+    BB_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_bytes));
+    pool_dev = dev;
+  }
   // kept-row ranks (exclusive scan of the keep mask, n_rows + 1 entries)
   uint32_t *rank = nullptr, *req = nullptr;
   void* tmp = nullptr;

@@ -264,3 +264,25 @@ def test_lane_encode_structured_fuzz(codec):
         want = zlib.compress(data, 6)
         assert got == want, (trial, n, len(got), len(want))
         assert dec(got, n) == data, (trial, n)
+
+
+def test_parallel_inflate_long_copy_chains(codec):
+    """Copy chains that run back across hundreds of 32 KiB resolution windows (periods of
+    7 B to 30 KB repeated for MiBs, with sparse literals) take the pointer-doubling rounds
+    before the chase; the output must still be exact, and corruption still caught."""
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    rng = random.Random(77)
+    for period, n, lit in ((4096, 4 << 20, 8), (30000, 6 << 20, 8), (7, 4 << 20, 6)):
+        buf = bytearray((rng.randbytes(period) * (n // period + 1))[:n])
+        for _ in range(n >> lit):  # sparse literals break some chains part-way
+            buf[rng.randrange(n)] = rng.randrange(256)
+        data = bytes(buf)
+        blob = zlib.compress(data, 6)
+        assert len(blob) >= 1 << 16  # the parallel decoder's range
+        before = _inflate_counts()
+        assert dec(blob, n) == data, (period, n)
+        assert _inflate_counts()[0] == before[0] + 1
+        bad = bytearray(blob)
+        bad[len(bad) // 2] ^= 0x10
+        with pytest.raises(codec.CorruptContainer):
+            dec(bytes(bad), n)
