@@ -1779,7 +1779,8 @@ __global__ void __launch_bounds__(32) k_resolve_sample(const PJob* __restrict__ 
                                                       const ExtEntry* __restrict__ ext,
                                                       const uint32_t* __restrict__ ext_cnt,
                                                       const uint32_t* __restrict__ extp,
-                                                      const uint8_t* __restrict__ wflag, unsigned long long* jstat) {
+                                                      const uint8_t* __restrict__ wflag, unsigned long long* jstat,
+                                                      uint32_t cap) {
   const uint32_t j = job_of_sub[blockIdx.x];
   const PJob J = jobs[j];
   const uint32_t c = fail[j] ? 0u : ext_cnt[blockIdx.x];
@@ -1789,7 +1790,9 @@ __global__ void __launch_bounds__(32) k_resolve_sample(const PJob* __restrict__ 
   uint32_t hops = 0, n = 0;
   for (uint32_t k = threadIdx.x * RJ_SAMPLE; k < c; k += 32 * RJ_SAMPLE) {
     uint32_t v = E[k].src, w, h = 1;
-    while (h < 4096 && WF[v / SUB] && (w = X[v]) != 0xFFFFFFFFu && w < v) v = w, h++;
+    // capped at twice the last round's threshold (cap): the gate needs no more, and
+    // the sampled chase is itself a dependent-load walk (133 hops mean on config3)
+    while (h < cap && WF[v / SUB] && (w = X[v]) != 0xFFFFFFFFu && w < v) v = w, h++;
     hops += h;
     n++;
   }
@@ -2283,7 +2286,7 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     if (jumps > 0) {
       BB_CUDA_TRY(cudaMemsetAsync(d_jstat, 0, sizeof(unsigned long long) * 2, st));
       k_resolve_sample<<<(unsigned)sub_job.size(), 32, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
-                                                                d_wflag, d_jstat);
+                                                                d_wflag, d_jstat, 8u << jumps);
       BB_LAUNCH_CHECK();
     }
     for (int r = 0; r < jumps; r++) {
