@@ -120,6 +120,25 @@ namespace {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Selects a device for the duration of an entry point and restores the caller's
+// current device on exit (a torchrun worker bound to GPU k must stay on GPU k).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+#define BB_DEVICE_GUARD(dev)                                                                  \
+  DeviceGuard bb_dg_(dev);                                                                    \
+  if (bb_dg_.err != cudaSuccess)                                                              \
+    return bb::fail(BB_CUDA_ERROR, "cudaSetDevice(%d): %s", (int)(dev), cudaGetErrorString(bb_dg_.err))
+
 uint64_t rd_u64(const uint8_t* p) {
   uint64_t v = 0;
   for (int i = 0; i < 8; i++) v |= (uint64_t)p[i] << (8 * i);
@@ -250,7 +269,7 @@ int bb_ipc_import(int device, const void* handle64, size_t offset, void** d_ptr,
     bb::set_error("ipc_import: null argument");
     return BB_INVALID_ARG;
   }
-  BB_CUDA_TRY(cudaSetDevice(device));
+  BB_DEVICE_GUARD(device);
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle64, sizeof h);
   void* base = nullptr;
@@ -293,7 +312,7 @@ const char* bb_stage_report(int reset) {
 
 int bb_ctx_create(bb_ctx** out, int device) {
   if (!out) return fail(BB_INVALID_ARG, "null ctx pointer");
-  BB_CUDA_TRY(cudaSetDevice(device));
+  BB_DEVICE_GUARD(device);
   bb_ctx* c = new bb_ctx();
   c->device = device;
   cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
@@ -309,7 +328,7 @@ int bb_ctx_create(bb_ctx** out, int device) {
 
 void bb_ctx_destroy(bb_ctx* c) {
   if (!c) return;
-  cudaSetDevice(c->device);
+  DeviceGuard g(c->device);
   deflate_engine_destroy(c->deflate);
   inflate_engine_destroy(c->inflate);
   if (c->own) cudaStreamDestroy(c->own);
@@ -346,6 +365,7 @@ int bb_compress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, const 
                       int split, uint8_t* const* d_out, const size_t* out_cap, size_t* out_len,
                       int* status, void* stream) {
   if (!ctx || count < 0) return fail(BB_INVALID_ARG, "bad arguments");
+  BB_DEVICE_GUARD(ctx->device);  // the stream and the engines belong to ctx->device
   cudaStream_t st = S(stream);
   int first = BB_OK;
   int rc = check_backend(backend);
@@ -428,6 +448,7 @@ int bb_decompress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, cons
                         uint8_t* const* d_out, const size_t* out_cap, size_t* out_len, int* status,
                         void* stream) {
   if (!ctx || count < 0) return fail(BB_INVALID_ARG, "bad arguments");
+  BB_DEVICE_GUARD(ctx->device);  // the stream and the engines belong to ctx->device
   cudaStream_t st = S(stream);
   std::vector<int> st_local(count > 0 ? count : 1);
   int* stv = status ? status : st_local.data();
@@ -534,6 +555,7 @@ int bb_backend_encode(bb_ctx* ctx, int backend, const uint8_t* d_in, size_t n, u
   int rc = check_backend(backend);
   if (rc) return rc;
   if (!ctx) return fail(BB_INVALID_ARG, "null ctx");
+  BB_DEVICE_GUARD(ctx->device);  // the stream and the engines belong to ctx->device
   cudaStream_t st = S(stream);
   if (backend == BB_BACKEND_IDENTITY) {
     if (out_cap < n) return fail(BB_INVALID_ARG, "output buffer too small");
@@ -558,6 +580,8 @@ int bb_backend_decode(bb_ctx* ctx, int backend, const uint8_t* d_in, size_t n, s
   int rc = check_backend(backend);
   if (rc) return rc;
   if ((rc = lane_precheck(backend, n, expected))) return rc;
+  if (!ctx) return fail(BB_INVALID_ARG, "null ctx");
+  BB_DEVICE_GUARD(ctx->device);
   cudaStream_t st = S(stream);
   if (backend == BB_BACKEND_IDENTITY) {
     if (n) BB_CUDA_TRY(cudaMemcpyAsync(d_out, d_in, n, cudaMemcpyDeviceToDevice, st));
@@ -584,7 +608,7 @@ static int to_device(bb_ctx* c, Workspace& w, const uint8_t* h, size_t n, uint8_
 int bb_compress_host(bb_ctx* c, const uint8_t* h_in, size_t n, int backend, int split, uint8_t* h_out,
                      size_t out_cap, size_t* out_len) {
   if (!c) return fail(BB_INVALID_ARG, "null ctx");
-  BB_CUDA_TRY(cudaSetDevice(c->device));
+  BB_DEVICE_GUARD(c->device);
   uint8_t *din, *dout;
   int rc = to_device(c, c->host_in, h_in, n, &din);
   if (rc) return rc;
@@ -604,17 +628,20 @@ int bb_compress_host(bb_ctx* c, const uint8_t* h_in, size_t n, int backend, int 
 int bb_decompress_host(bb_ctx* c, const uint8_t* h_in, size_t n, uint8_t* h_out, size_t out_cap,
                        size_t* out_len) {
   if (!c) return fail(BB_INVALID_ARG, "null ctx");
-  BB_CUDA_TRY(cudaSetDevice(c->device));
-  uint8_t* din;
-  int rc = to_device(c, c->host_in, h_in, n, &din);
-  if (rc) return rc;
-  size_t need = 0;
-  rc = bb_decompress(c, din, n, nullptr, 0, &need, c->own);
+  if (!h_in && n) return fail(BB_INVALID_ARG, "null input");
+  // parse_container + the decode plan run on the host copy: a size query uploads nothing
+  Header hd;
+  uint64_t need = 0;
+  int rc = parse_header(h_in, n, &hd);
+  if (!rc) rc = plan_decode(hd, &need);
   if (rc) return rc;
   if (!h_out) {
     *out_len = need;
     return BB_OK;
   }
+  BB_DEVICE_GUARD(c->device);
+  uint8_t* din;
+  if ((rc = to_device(c, c->host_in, h_in, n, &din))) return rc;
   if (need > out_cap) return fail(BB_INVALID_ARG, "output buffer too small");
   if ((rc = c->host_out.reserve(need + 64))) return rc;
   uint8_t* dout = static_cast<uint8_t*>(c->host_out.base);
@@ -632,7 +659,7 @@ int bb_backend_encode_host(bb_ctx* c, int backend, const uint8_t* h_in, size_t n
   if (!c) return fail(BB_INVALID_ARG, "null ctx");
   int rc = check_backend(backend);
   if (rc) return rc;
-  BB_CUDA_TRY(cudaSetDevice(c->device));
+  BB_DEVICE_GUARD(c->device);
   uint8_t* din;
   if ((rc = to_device(c, c->host_in, h_in, n, &din))) return rc;
   size_t bound = bb_backend_bound(backend, n);
@@ -653,7 +680,7 @@ int bb_backend_decode_host(bb_ctx* c, int backend, const uint8_t* h_in, size_t n
   int rc = check_backend(backend);
   if (rc) return rc;
   if ((rc = lane_precheck(backend, n, expected))) return rc;
-  BB_CUDA_TRY(cudaSetDevice(c->device));
+  BB_DEVICE_GUARD(c->device);
   uint8_t* din;
   if ((rc = to_device(c, c->host_in, h_in, n, &din))) return rc;
   if ((rc = c->host_out.reserve(expected + 64))) return rc;
@@ -667,7 +694,7 @@ int bb_backend_decode_host(bb_ctx* c, int backend, const uint8_t* h_in, size_t n
 int bb_split_host(bb_ctx* c, const uint8_t* h_stream, size_t n, uint8_t* h_high, uint8_t* h_low) {
   if (!c) return fail(BB_INVALID_ARG, "null ctx");
   if (n % 2) return fail(BB_ODD_LENGTH, "byte_split: stream length must be even, got %zu", n);
-  BB_CUDA_TRY(cudaSetDevice(c->device));
+  BB_DEVICE_GUARD(c->device);
   uint8_t* din;
   int rc = to_device(c, c->host_in, h_stream, n, &din);
   if (rc) return rc;
@@ -685,7 +712,7 @@ int bb_split_host(bb_ctx* c, const uint8_t* h_stream, size_t n, uint8_t* h_high,
 
 int bb_merge_host(bb_ctx* c, const uint8_t* h_high, const uint8_t* h_low, size_t count, uint8_t* h_out) {
   if (!c) return fail(BB_INVALID_ARG, "null ctx");
-  BB_CUDA_TRY(cudaSetDevice(c->device));
+  BB_DEVICE_GUARD(c->device);
   int rc = c->host_in.reserve(2 * count + 64);
   if (rc) return rc;
   uint8_t* hi = static_cast<uint8_t*>(c->host_in.base);
@@ -704,7 +731,7 @@ int bb_merge_host(bb_ctx* c, const uint8_t* h_high, const uint8_t* h_low, size_t
 
 int bb_histogram256_host(bb_ctx* c, const uint8_t* h_data, size_t n, uint64_t* h_counts) {
   if (!c) return fail(BB_INVALID_ARG, "null ctx");
-  BB_CUDA_TRY(cudaSetDevice(c->device));
+  BB_DEVICE_GUARD(c->device);
   uint8_t* din;
   int rc = to_device(c, c->host_in, h_data, n, &din);
   if (rc) return rc;

@@ -34,7 +34,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
-#include <unistd.h>
+#include <mutex>
 
 #include <cstring>
 #include <vector>
@@ -720,16 +720,10 @@ __global__ void __launch_bounds__(ND_THREADS) k_decode_nodes(const PJob* __restr
 #define WD_WARPS_OVR 2
 #endif
 constexpr int WD_WARPS = WD_WARPS_OVR;
-__device__ unsigned long long g_wd[8];  // watchdog trips per loop site (debug)
-__device__ unsigned* g_prog;             // debug: progress words in mapped host memory (or null)
-#ifdef BB_PROG_DEBUG  // progress words for hang diagnosis (kept out of the hot loops otherwise)
-#define PROG(d, lane, ph, x) \
-  if (g_prog) ((volatile unsigned*)g_prog)[(d) * 32 + (lane)] = ((ph) << 24) | ((unsigned)(x) & 0xffffff)
-#else
+__device__ unsigned long long g_wd[8];  // loop-guard trips per site (corrupt-stream safety limits)
 #define PROG(d, lane, ph, x) \
   do {                       \
   } while (0)
-#endif
 #define WD_GUARD(site, it, limit, action)        \
   if (++(it) > (limit)) {                        \
     atomicAdd(&g_wd[site], 1ull);                \
@@ -1004,9 +998,7 @@ __global__ void __launch_bounds__(32 * WD_WARPS, DS_MINB) k_dyn_scan(const PJob*
   uint64_t real_err = lane == 0 ? err_at : NONE64;
   uint64_t ev_out = eob_out, ev_nm = eob_nm;
   uint64_t used = lane == 0 ? d0 : NONE64 - 1;
-  if (lane == 0) atomicAdd(&g_wd[5], 1ull);  // dynamic blocks scanned
   for (int iter = 0; iter < 33; iter++) {
-    if (lane == 0) atomicAdd(&g_wd[6], 1ull);  // fix-up iterations
     PROG(d, lane, 4, iter);
     uint64_t entry = __shfl_up_sync(0xffffffffu, F, 1);
     bool blocked = __shfl_up_sync(0xffffffffu, (int)(real_eob != NONE64 || real_err != NONE64), 1);
@@ -1932,6 +1924,15 @@ __global__ void k_adler_check(const PJob* __restrict__ jobs, int njobs, const ui
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= njobs || fail[j]) return;
   const PJob J = jobs[j];
+  // the zlib header (inflate.c HEAD state, as inflate_stream checks it): decoding starts at
+  // bit 16, so a bad CMF/FLG must fail here and go to the exact decoder for its status
+  {
+    const uint32_t cmf = J.src[0], flg = J.src[1];
+    if (((cmf << 8) | flg) % 31u != 0 || (cmf & 0x0f) != 8 || (cmf >> 4) > 7 || (flg & 0x20)) {
+      fail[j] = 1;
+      return;
+    }
+  }
   uint64_t nch = (J.expected + PA_CHUNK - 1) / PA_CHUNK;
   uint64_t TA = 0, TB = 0;
   for (uint64_t c = 0; c < nch; c++) {
@@ -1973,15 +1974,23 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   if (!nj) return BB_OK;
   StageTimer T(st);
   T.mark("inflate.setup");
-  static bool attr = false;
+  // shared-memory opt-ins are per device: one flag per device, set under a lock
+  static std::mutex attr_mu;
+  static bool attr_done[64] = {};
   size_t nd_smem = sizeof(Tables) * ND_THREADS;
-  if (!attr) {
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
-    BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(sizeof(WarpSm) * WD_WARPS)));
-    attr = true;
+  int dev = 0;
+  BB_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return BB_INVALID_ARG;
+  {
+    std::lock_guard<std::mutex> attr_lock(attr_mu);
+    if (!attr_done[dev]) {
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(WarpSm) * WD_WARPS)));
+      attr_done[dev] = true;
+    }
   }
   std::vector<PJob> J(nj);
   std::vector<uint32_t> sub_job, chunk_job, chunk_base(nj);
@@ -2180,27 +2189,9 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   k_decode_nodes<<<(nnodes + ND_THREADS - 1) / ND_THREADS, ND_THREADS, nd_smem, st>>>(d_jobs, d_node_job, nnodes,
                                                                                       d_nodes);
   BB_LAUNCH_CHECK();
-  unsigned* h_prog = nullptr;
-  if (debug_sync() && ndyn_total) {
-    cudaHostAlloc(reinterpret_cast<void**>(&h_prog), 4ull * 32 * ndyn_total, cudaHostAllocMapped);
-    memset(h_prog, 0, 4ull * 32 * ndyn_total);
-    unsigned* dp = nullptr;
-    cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), h_prog, 0);
-    cudaMemcpyToSymbol(g_prog, &dp, sizeof(dp));
-  }
   if (ndyn_total) {
     k_dyn_scan<<<(ndyn_total + WD_WARPS - 1) / WD_WARPS, 32 * WD_WARPS, sizeof(WarpSm) * WD_WARPS, st>>>(
         d_jobs, d_node_job, d_dyn_nodes, ndyn_total, d_nodes, d_dtabs, d_plans, d_extra);
-    for (int sec = 0; h_prog && sec < 6; sec++) {
-      if (cudaStreamQuery(st) == cudaSuccess) break;
-      usleep(1000000);
-      fprintf(stderr, "[bb] k_dyn_scan progress after %d s:\n", sec + 1);
-      for (uint32_t d = 0; d < ndyn_total; d++) {
-        fprintf(stderr, "  blk %u:", d);
-        for (int l = 0; l < 32; l++) fprintf(stderr, " %x", h_prog[d * 32 + l]);
-        fprintf(stderr, "\n");
-      }
-    }
     BB_LAUNCH_CHECK();
   }
   T.mark("inflate.link_chain");
@@ -2285,6 +2276,9 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     static const int jumps = std::min(RJ_MAX, getenv("BB_RESOLVE_JUMPS") ? atoi(getenv("BB_RESOLVE_JUMPS")) : RJ_ROUNDS);
     if (jumps > 0) {
       BB_CUDA_TRY(cudaMemsetAsync(d_jstat, 0, sizeof(unsigned long long) * 2, st));
+      // each sampled chase is capped at 8 << jumps hops = 4x the last round's threshold (round r runs
+      // while the mean exceeds 4 << r); the capped mean is biased low, so a long-chain workload can
+      // run fewer rounds than it needs -- the chase after the rounds stays exact either way
       k_resolve_sample<<<(unsigned)sub_job.size(), 32, 0, st>>>(d_jobs, d_sub_job, d_fail, d_ext, d_ext_cnt, d_extp,
                                                                 d_wflag, d_jstat, 8u << jumps);
       BB_LAUNCH_CHECK();
@@ -2322,6 +2316,6 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
 
 }  // namespace bb
 
-extern "C" BB_API void bb_debug_inflate_watchdog(unsigned long long* out8) {
+extern "C" BB_API void bb_debug_inflate_guards(unsigned long long* out8) {
   cudaMemcpyFromSymbol(out8, bb::par::g_wd, sizeof(unsigned long long) * 8);
 }

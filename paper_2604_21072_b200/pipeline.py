@@ -79,6 +79,15 @@ def parse_frame_header(h: bytes):
     return msg_type, batch_id, micro, flags, plen
 
 
+def read_frame_header(h: bytes):
+    """read_frame's header rules (wire.cpp:250-267): decode_frame's checks plus the 1 GiB cap on
+    the declared payload length, checked before any payload byte is received."""
+    msg_type, batch_id, micro, flags, plen = parse_frame_header(h)
+    if plen > MAX_PAYLOAD:
+        raise FrameCorrupt("frame: implausible payload length")
+    return msg_type, batch_id, micro, flags, plen
+
+
 def decode_frame(data: bytes) -> WireFrame:
     data = bytes(data)
     msg_type, batch_id, micro, flags, plen = parse_frame_header(data)
@@ -207,7 +216,14 @@ class PeerInbox:
     a small "doorbell" that also orders buffer reuse (slot k % slots is rewritten
     only after the receiver has posted the doorbell of the step after k, i.e.
     finished decoding k).  Frame m of a step sits at a fixed offset: 20-byte BBF1
-    header, then the container."""
+    header, then the container.
+
+    Back-pressure: the doorbell alone only orders a stage after its *previous* stage,
+    and NCCL's small sends complete before the matching receive is posted, so in a ring
+    of three or more GPUs a stage could run ahead of its next stage and rewrite a slot
+    still being decoded.  After decoding step k a stage therefore acks k to its previous
+    stage (release()); a stage waits for its next stage's ack of step k - slots before the
+    codec writes that slot again (out_ptrs())."""
 
     def __init__(self, caps, device, slots: int = 2):
         import ctypes as C
@@ -246,9 +262,15 @@ class PeerInbox:
             self.out_ptr.append(p.value)
             self.out_base.append(base.value)
         torch.cuda.set_device(device)
+        self.acks = {}  # step -> (works, tensors) of the ack exchange issued after decoding step
 
     def out_ptrs(self, slot: int):
-        """Container destinations inside the next stage's inbox (after each frame header)."""
+        """Container destinations inside the next stage's inbox (after each frame header).
+        Blocks (stream-ordered) until the next stage acked the previous use of the slot."""
+        pending = self.acks.pop(slot - self.slots, None)
+        if pending is not None:
+            for w in pending[0]:
+                w.wait()
         base = self.out_ptr[slot % self.slots]
         return [base + o + FRAME_HEADER for o in self.offsets], self.caps
 
@@ -271,7 +293,25 @@ class PeerInbox:
         ib = self.inbox[slot % self.slots]
         return [ib[o:o + FRAME_HEADER + int(n)] for o, n in zip(self.offsets, got.tolist())]
 
+    def release(self, slot: int):
+        """This stage finished decoding `slot`'s frames (stream-ordered): ack it to the
+        previous stage and receive the next stage's ack of the same step (one symmetric
+        NCCL group, so the ring cannot deadlock)."""
+        dist, torch = self.dist, self.torch
+        ack = torch.full((1,), slot, dtype=torch.int64, device=self.device)
+        got = torch.empty(1, dtype=torch.int64, device=self.device)
+        works = dist.batch_isend_irecv([dist.P2POp(dist.isend, ack, self.prev),
+                                        dist.P2POp(dist.irecv, got, self.next)])
+        self.acks[slot] = (works, (ack, got))
+
+    def drain(self):
+        for works, _ in self.acks.values():
+            for w in works:
+                w.wait()
+        self.acks.clear()
+
     def close(self):
+        self.drain()
         for b in self.out_base:
             self.L.bb_ipc_close(b)
         self.out_base, self.out_ptr = [], []
@@ -295,7 +335,7 @@ def open_frames(frames):
     heads = torch.cat([f[:FRAME_HEADER] for f in frames]).cpu().numpy().tobytes()
     meta, payloads = [], []
     for m, f in enumerate(frames):
-        t, b, mi, fl, plen = parse_frame_header(heads[FRAME_HEADER * m:FRAME_HEADER * (m + 1)])
+        t, b, mi, fl, plen = read_frame_header(heads[FRAME_HEADER * m:FRAME_HEADER * (m + 1)])
         if f.numel() != FRAME_HEADER + plen:
             raise FrameCorrupt("frame: payload length does not match the header")
         meta.append((t, b, mi, fl))

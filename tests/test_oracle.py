@@ -174,3 +174,21 @@ def test_uncompress_fuzz_matches_libz(oracle):
             assert gok and got == want
         elif not ok:
             assert not gok
+
+
+def test_oracle_restatement_at_full_config2_size(oracle):
+    """The C restatement (oracle/zlib6.c) reproduces the reference's container of a whole config2
+    micro-batch (64 MiB bf16, seed 1000): the full-size golden is pinned by two implementations."""
+    import hashlib
+    import json
+    import os
+
+    from paper_2604_21072_b200 import workloads as W
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fullsize_golden.json")))
+    (e,) = [g for g in gold["entries"] if g["config"] == "config2" and g["index"] == 0]
+    syn = lambda n, s, bf16: oracle.synth_bf16(n, s) if bf16 else oracle.synth_fp16(n, s)  # noqa: E731
+    data = W.config2_micro(syn, 0, 0)
+    assert hashlib.sha256(data).hexdigest() == e["raw_sha256"]
+    c = oracle.compress(data, 1, True)
+    assert len(c) == e["len"] == 47056924
+    assert hashlib.sha256(c).hexdigest() == e["sha256"]

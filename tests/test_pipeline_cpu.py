@@ -115,3 +115,12 @@ def test_stage_ring_gloo(ring):
     # rank 1 always receives rank 0's frames; rank 0 receives rank 1's only in ring mode
     assert res[1] == [(0, m, bytes([0] * (m + 1))) for m in range(3)]
     assert res[0] == ([(1, m, bytes([1] * (m + 1))) for m in range(3)] if ring else [])
+
+
+def test_read_frame_rejects_payloads_over_one_gib():
+    """wire.cpp:260: read_frame refuses a declared payload_len > 1 GiB before reading it."""
+    from paper_2604_21072_b200.pipeline import FrameCorrupt, MAX_PAYLOAD, frame_header, read_frame_header
+    ok = frame_header(0, 1, 0, 3, MAX_PAYLOAD)
+    assert read_frame_header(ok)[4] == MAX_PAYLOAD
+    with pytest.raises(FrameCorrupt, match="implausible payload length"):
+        read_frame_header(frame_header(0, 1, 0, 3, MAX_PAYLOAD + 1))
