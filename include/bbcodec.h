@@ -71,6 +71,9 @@ BB_API void bb_ctx_destroy(bb_ctx* ctx);
 /* ---- lanes (device) --------------------------------------------------- */
 BB_API int bb_split(const uint8_t* d_stream, size_t n_bytes, uint8_t* d_high, uint8_t* d_low, void* stream);
 BB_API int bb_merge(const uint8_t* d_high, const uint8_t* d_low, size_t count, uint8_t* d_stream, void* stream);
+/* *equal = (d_a[0:n] == d_b[0:n]) on ctx's device (the sink's bit-exact reassembly check,
+ * wire.cpp:555-560); synchronizes the stream. */
+BB_API int bb_equal(bb_ctx* ctx, const uint8_t* d_a, const uint8_t* d_b, size_t n, int* equal, void* stream);
 /* 256 u64 counts, overwritten */
 BB_API int bb_histogram256(const uint8_t* d_data, size_t n, uint64_t* d_counts, void* stream);
 

@@ -24,7 +24,7 @@ EXPORTS = [
     "bb_split_host", "bb_merge_host", "bb_histogram256_host", "bb_kernel_launches",
     "bb_stage_timing", "bb_stage_report", "bb_packed_bound", "bb_pack_sd", "bb_unpack_sd",
     "bb_gather_pages", "bb_enable_peer_access", "bb_ipc_export", "bb_ipc_import", "bb_ipc_close",
-    "bb_copy_h2d",
+    "bb_copy_h2d", "bb_equal",
 ]
 
 _u8p = C.c_void_p
@@ -52,6 +52,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         L.bb_split.argtypes = [_u8p, _sz, _u8p, _u8p, C.c_void_p]
         L.bb_merge.argtypes = [_u8p, _u8p, _sz, _u8p, C.c_void_p]
         L.bb_histogram256.argtypes = [_u8p, _sz, _u8p, C.c_void_p]
+        L.bb_equal.argtypes = [C.c_void_p, _u8p, _u8p, _sz, C.POINTER(C.c_int), C.c_void_p]
         L.bb_compress_bound.restype = _sz
         L.bb_compress_bound.argtypes = [_sz, C.c_int, C.c_int]
         L.bb_backend_bound.restype = _sz

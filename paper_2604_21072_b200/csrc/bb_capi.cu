@@ -114,6 +114,8 @@ struct bb_ctx {
   Workspace host_in, host_out; // device copies for the *_host calls
   DeflateEngine* deflate = nullptr;
   InflateEngine* inflate = nullptr;
+  unsigned int* d_flag = nullptr;  // bb_equal's result word (device) and its pinned host copy
+  unsigned int* h_flag = nullptr;
 };
 
 namespace {
@@ -332,6 +334,8 @@ void bb_ctx_destroy(bb_ctx* c) {
   deflate_engine_destroy(c->deflate);
   inflate_engine_destroy(c->inflate);
   if (c->own) cudaStreamDestroy(c->own);
+  if (c->d_flag) cudaFree(c->d_flag);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
   delete c;
 }
 
@@ -344,6 +348,20 @@ int bb_split(const uint8_t* d_stream, size_t n, uint8_t* d_high, uint8_t* d_low,
 int bb_merge(const uint8_t* d_high, const uint8_t* d_low, size_t count, uint8_t* d_out, void* stream) {
   if (count && (!d_high || !d_low || !d_out)) return fail(BB_INVALID_ARG, "null pointer");
   return launch_merge(d_high, d_low, count, d_out, S(stream));
+}
+
+int bb_equal(bb_ctx* ctx, const uint8_t* d_a, const uint8_t* d_b, size_t n, int* equal, void* stream) {
+  if (!ctx || !equal || (n && (!d_a || !d_b))) return fail(BB_INVALID_ARG, "null pointer");
+  BB_DEVICE_GUARD(ctx->device);
+  if (!ctx->h_flag)
+    BB_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_flag), sizeof(unsigned int), cudaHostAllocDefault));
+  if (!ctx->d_flag) BB_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&ctx->d_flag), sizeof(unsigned int)));
+  int rc = launch_differ(d_a, d_b, n, ctx->d_flag, S(stream));
+  if (rc) return rc;
+  BB_CUDA_TRY(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(unsigned int), cudaMemcpyDeviceToHost, S(stream)));
+  BB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  *equal = *ctx->h_flag == 0;
+  return BB_OK;
 }
 
 int bb_histogram256(const uint8_t* d, size_t n, uint64_t* d_counts, void* stream) {

@@ -12,6 +12,7 @@ int launch_identity_container(const uint8_t* in, uint64_t n, int split, uint8_t*
 int launch_split(const uint8_t* in, uint64_t count, uint8_t* hi, uint8_t* lo, cudaStream_t st);
 int launch_merge(const uint8_t* hi, const uint8_t* lo, uint64_t count, uint8_t* out, cudaStream_t st);
 int launch_hist256(const uint8_t* in, uint64_t n, unsigned long long* counts, cudaStream_t st);
+int launch_differ(const uint8_t* a, const uint8_t* b, uint64_t n, unsigned int* differ, cudaStream_t st);
 
 // Grow-only device scratch owned by a context.
 struct Workspace {

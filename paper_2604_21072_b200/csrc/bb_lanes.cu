@@ -189,7 +189,38 @@ __global__ void __launch_bounds__(256) k_hist256(const uint8_t* __restrict__ in,
   }
 }
 
+// a != b anywhere in [0, n): 16-byte loads where both sides share alignment, bytes otherwise
+__global__ void __launch_bounds__(256) k_differ(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
+                                                uint64_t n, unsigned int* __restrict__ differ) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uintptr_t pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+  bool d = false;
+  if (((pa ^ pb) & 15) == 0) {
+    uint64_t head = (16 - (pa & 15)) & 15;
+    if (head > n) head = n;
+    const uint64_t vecs = (n - head) / 16;
+    for (uint64_t v = tid; v < vecs; v += stride) {
+      uint4 x = ldg16(a + head + 16 * v), y = ldg16(b + head + 16 * v);
+      d |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+    }
+    for (uint64_t i = tid; i < head; i += stride) d |= a[i] != b[i];
+    for (uint64_t i = head + 16 * vecs + tid; i < n; i += stride) d |= a[i] != b[i];
+  } else {
+    for (uint64_t i = tid; i < n; i += stride) d |= a[i] != b[i];
+  }
+  if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) atomicOr(differ, 1u);
+}
+
 }  // namespace
+
+int launch_differ(const uint8_t* a, const uint8_t* b, uint64_t n, unsigned int* differ, cudaStream_t st) {
+  BB_CUDA_TRY(cudaMemsetAsync(differ, 0, sizeof(unsigned int), st));
+  if (n == 0) return BB_OK;
+  k_differ<<<grid_for(n / 16 + 1, 256, 8), 256, 0, st>>>(a, b, n, differ);
+  BB_LAUNCH_CHECK();
+  return BB_OK;
+}
 
 int launch_identity_container(const uint8_t* in, uint64_t n, int split, uint8_t* out,
                               cudaStream_t st) {
