@@ -114,6 +114,7 @@ struct bb_ctx {
   Workspace host_in, host_out; // device copies for the *_host calls
   DeflateEngine* deflate = nullptr;
   InflateEngine* inflate = nullptr;
+  HostStager io;                   // pageable host buffers of the *_host entry points
   unsigned int* d_flag = nullptr;  // bb_equal's result word (device) and its pinned host copy
   unsigned int* h_flag = nullptr;
 };
@@ -619,8 +620,7 @@ static int to_device(bb_ctx* c, Workspace& w, const uint8_t* h, size_t n, uint8_
   int r = w.reserve(n + 64);
   if (r) return r;
   *d = static_cast<uint8_t*>(w.base);
-  if (n) BB_CUDA_TRY(cudaMemcpyAsync(*d, h, n, cudaMemcpyHostToDevice, c->own));
-  return BB_OK;
+  return c->io.h2d(*d, h, n, c->own);
 }
 
 int bb_compress_host(bb_ctx* c, const uint8_t* h_in, size_t n, int backend, int split, uint8_t* h_out,
@@ -637,7 +637,7 @@ int bb_compress_host(bb_ctx* c, const uint8_t* h_in, size_t n, int backend, int 
   rc = bb_compress(c, din, n, backend, split, dout, bound, &len, c->own);
   if (rc) return rc;
   if (len > out_cap) return fail(BB_INVALID_ARG, "output buffer too small");
-  if (len) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, len, cudaMemcpyDeviceToHost, c->own));
+  if (len && (rc = c->io.d2h(h_out, dout, len, c->own))) return rc;
   BB_CUDA_TRY(cudaStreamSynchronize(c->own));
   *out_len = len;
   return BB_OK;
@@ -666,7 +666,7 @@ int bb_decompress_host(bb_ctx* c, const uint8_t* h_in, size_t n, uint8_t* h_out,
   size_t len = 0;
   rc = bb_decompress(c, din, n, dout, need, &len, c->own);
   if (rc) return rc;
-  if (len) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, len, cudaMemcpyDeviceToHost, c->own));
+  if (len && (rc = c->io.d2h(h_out, dout, len, c->own))) return rc;
   BB_CUDA_TRY(cudaStreamSynchronize(c->own));
   *out_len = len;
   return BB_OK;
@@ -686,7 +686,7 @@ int bb_backend_encode_host(bb_ctx* c, int backend, const uint8_t* h_in, size_t n
   size_t len = 0;
   if ((rc = bb_backend_encode(c, backend, din, n, dout, bound, &len, c->own))) return rc;
   if (len > out_cap) return fail(BB_INVALID_ARG, "output buffer too small");
-  if (len) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, len, cudaMemcpyDeviceToHost, c->own));
+  if (len && (rc = c->io.d2h(h_out, dout, len, c->own))) return rc;
   BB_CUDA_TRY(cudaStreamSynchronize(c->own));
   *out_len = len;
   return BB_OK;
@@ -704,7 +704,7 @@ int bb_backend_decode_host(bb_ctx* c, int backend, const uint8_t* h_in, size_t n
   if ((rc = c->host_out.reserve(expected + 64))) return rc;
   uint8_t* dout = static_cast<uint8_t*>(c->host_out.base);
   if ((rc = bb_backend_decode(c, backend, din, n, expected, dout, c->own))) return rc;
-  if (expected) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, expected, cudaMemcpyDeviceToHost, c->own));
+  if (expected && (rc = c->io.d2h(h_out, dout, expected, c->own))) return rc;
   BB_CUDA_TRY(cudaStreamSynchronize(c->own));
   return BB_OK;
 }
@@ -742,7 +742,7 @@ int bb_merge_host(bb_ctx* c, const uint8_t* h_high, const uint8_t* h_low, size_t
   if ((rc = c->host_out.reserve(2 * count + 64))) return rc;
   uint8_t* dout = static_cast<uint8_t*>(c->host_out.base);
   if ((rc = launch_merge(hi, lo, count, dout, c->own))) return rc;
-  if (count) BB_CUDA_TRY(cudaMemcpyAsync(h_out, dout, 2 * count, cudaMemcpyDeviceToHost, c->own));
+  if (count && (rc = c->io.d2h(h_out, dout, 2 * count, c->own))) return rc;
   BB_CUDA_TRY(cudaStreamSynchronize(c->own));
   return BB_OK;
 }

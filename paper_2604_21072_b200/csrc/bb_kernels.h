@@ -12,6 +12,21 @@ int launch_identity_container(const uint8_t* in, uint64_t n, int split, uint8_t*
 int launch_split(const uint8_t* in, uint64_t count, uint8_t* hi, uint8_t* lo, cudaStream_t st);
 int launch_merge(const uint8_t* hi, const uint8_t* lo, uint64_t count, uint8_t* out, cudaStream_t st);
 int launch_hist256(const uint8_t* in, uint64_t n, unsigned long long* counts, cudaStream_t st);
+// Staged pageable <-> device copies of the host-buffer entry points (bb_hostio.cu):
+// 4 MiB chunks through NB pinned buffers, host-side copies split across a worker pool.
+struct HostStager {
+  static constexpr int NB = 4;
+  static constexpr size_t CHUNK = size_t(4) << 20;
+  static constexpr size_t SMALL = size_t(1) << 20;  // below: one plain cudaMemcpyAsync
+  uint8_t* buf[NB] = {};
+  cudaEvent_t ev[NB] = {};
+  ~HostStager();
+  int ready();
+  // stream-ordered: h_src may be reused on return (its bytes are in the pinned buffers or on the device)
+  int h2d(uint8_t* d_dst, const uint8_t* h_src, size_t n, cudaStream_t st);
+  // returns when h_dst holds the bytes
+  int d2h(uint8_t* h_dst, const uint8_t* d_src, size_t n, cudaStream_t st);
+};
 int launch_differ(const uint8_t* a, const uint8_t* b, uint64_t n, unsigned int* differ, cudaStream_t st);
 
 // Grow-only device scratch owned by a context.
