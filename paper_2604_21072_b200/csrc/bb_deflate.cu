@@ -30,6 +30,7 @@
 //      k_adler*       Adler-32 (chunk sums + ordered combine), zlib header/trailer,
 //      k_finalize     BBC1 header
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -731,6 +732,262 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
       prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// K3S + K4S: match profiles over BUCKET-SORTED chains (variant, BB_K4_SORTED=1).
+//
+// zlib's hash chain of position p is the list of earlier positions with the same
+// 15-bit hash, most recent first (parse-independent, see K3).  A stable sort of
+// all positions by (lane, hash) lays every chain out contiguously: p's t-th
+// candidate is simply the sorted entry t places before p's own.  K4S gives each
+// thread one sorted entry, so the 32 lanes of a warp are 32 consecutive entries
+// and at chain step t they read 32 consecutive candidate records from shared
+// memory -- conflict-free, with no dependent link loads.  A record is the 8
+// bytes starting at the candidate, so the quick reject and the match length up
+// to 8 bytes come from one 64-bit load: x = cand ^ own, the candidate can beat
+// best only if bytes 0..best of x are zero, and the length is ctz(x) / 8.
+// Longer matches extend from the lane's bytes in global memory (rare on
+// activation planes).  The chain budget (32 / 128 candidates), the distance rule
+// (the head at <= MAX_DIST, later entries < MAX_DIST, position 0 never a
+// source), nice_match and the first-maximum rule are exactly K4's, so the
+// profiles are bit-identical (tests/test_gpu_deflate.py compares both with the
+// oracle's orc_match_profile).
+//
+//   k_sort_keys      key = lane << 16 | hash(p) (0xffff: fewer than 3 bytes left,
+//                    never inserted), value = p
+//   cub radix sort   stable: positions stay ascending inside a bucket
+//   k_profile_sorted CTA per KS_T sorted entries; stages the KS_H entries before
+//                    them (the longest chain a thread can walk) with their bytes
+constexpr uint32_t KS_NOHASH = 0xffffu;
+constexpr int KS_T = 1024;  // sorted entries (threads) per CTA
+constexpr int KS_H = 128;   // history entries staged before them (MAX_CHAIN)
+
+// 8 bytes starting at src + q (bytes at or past n read as 0)
+__device__ __forceinline__ uint64_t ks_load8(const uint8_t* src, uint64_t n, uint64_t q) {
+  const uint64_t a = q & ~uint64_t(7);
+  const uint32_t sh = (uint32_t)(q & 7) * 8;
+  const bool aligned_src = (reinterpret_cast<uintptr_t>(src) & 7) == 0;
+  if (aligned_src && a + 16 <= n) {
+    const uint64_t lo = __ldg(reinterpret_cast<const unsigned long long*>(src + a));
+    if (!sh) return lo;
+    const uint64_t hi = __ldg(reinterpret_cast<const unsigned long long*>(src + a + 8));
+    return (lo >> sh) | (hi << (64 - sh));
+  }
+  uint64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++)
+    if (q + k < n) v |= (uint64_t)__ldg(src + q + k) << (8 * k);
+  return v;
+}
+
+// grid (chunks, lanes): KS_KP positions per thread, keys = 15-bit hash (KS_NOHASH when fewer
+// than 3 bytes remain: never inserted, never searched), values = position
+constexpr int KS_KP = 8;
+__global__ void __launch_bounds__(256) k_sort_keys(const LaneDev* __restrict__ lanes,
+                                                   const uint64_t* __restrict__ lane_prefix,
+                                                   uint16_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const LaneDev L = lanes[blockIdx.y];
+  const uint64_t o = lane_prefix[blockIdx.y];
+  for (uint64_t p0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * KS_KP; p0 < L.n;
+       p0 += (uint64_t)gridDim.x * blockDim.x * KS_KP) {
+    const uint64_t a = ks_load8(L.src, L.n, p0), b = ks_load8(L.src, L.n, p0 + 8);
+#pragma unroll
+    for (int k = 0; k < KS_KP; k++) {
+      const uint64_t p = p0 + k;
+      if (p >= L.n) break;
+      const uint32_t b0 = (uint32_t)(a >> (8 * k)) & 0xff;
+      const uint32_t b1 = (uint32_t)(k + 1 < 8 ? a >> (8 * (k + 1)) : b >> (8 * (k - 7))) & 0xff;
+      const uint32_t b2 = (uint32_t)(k + 2 < 8 ? a >> (8 * (k + 2)) : b >> (8 * (k - 6))) & 0xff;
+      const uint32_t h = p + MIN_MATCH <= L.n ? ((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fffu : KS_NOHASH;
+      keys[o + p] = (uint16_t)h;
+      vals[o + p] = (uint32_t)p;
+    }
+  }
+}
+
+// common-prefix length of src[c..] and src[p..] from byte `from` (bytes below it match), capped at maxl
+__device__ __noinline__ uint32_t ks_extend(const uint8_t* src, uint64_t n, uint64_t c, uint64_t p, uint32_t from,
+                                           uint32_t maxl) {
+  uint32_t len = from;
+  while (len < maxl) {
+    const uint64_t x = ks_load8(src, n, c + len) ^ ks_load8(src, n, p + len);
+    if (x) {
+      len += (uint32_t)(__ffsll((long long)x) - 1) >> 3;
+      break;
+    }
+    len += 8;
+  }
+  return min(len, maxl);
+}
+
+__device__ __forceinline__ uint32_t ks_ctz(uint32_t x) {  // x != 0
+  uint32_t r;
+  asm("brev.b32 %0, %1;" : "=r"(r) : "r"(x));
+  asm("bfind.shiftamt.u32 %0, %0;" : "+r"(r));
+  return r;
+}
+
+constexpr int KS_B = 8;    // chain steps per batch (the quick tests of a batch are branch-free)
+constexpr int KS_PAD = 8;  // staged records before the window: a batch may overrun the chain
+
+__global__ void __launch_bounds__(KS_T, 1) k_profile_sorted(const LaneDev* __restrict__ lanes,
+                                                            const uint64_t* __restrict__ lane_prefix,
+                                                            const uint16_t* __restrict__ skeys,
+                                                            const uint32_t* __restrict__ spos,
+                                                            uint2* __restrict__ prof, int with_bytes) {
+  __shared__ uint64_t sb[KS_PAD + KS_H + KS_T];  // 8 bytes at each staged entry's position
+  __shared__ uint32_t sk[KS_H + KS_T];           // its hash (KS_NOHASH outside the lane)
+  __shared__ uint32_t sp[KS_H + KS_T];           // its position
+  const LaneDev L = lanes[blockIdx.y];
+  const uint64_t n = L.n;
+  const uint64_t j0 = (uint64_t)blockIdx.x * KS_T;  // lane-relative sorted index
+  if (j0 >= n) return;
+  const uint16_t* keys = skeys + lane_prefix[blockIdx.y];
+  const uint32_t* poss = spos + lane_prefix[blockIdx.y];
+  const int64_t base = (int64_t)j0 - KS_H;  // staged index i <-> sorted entry base + i
+  if (threadIdx.x < KS_PAD) sb[threadIdx.x] = ~0ull;
+  for (int i = threadIdx.x; i < KS_H + KS_T; i += blockDim.x) {
+    const int64_t j = base + i;
+    uint32_t k = KS_NOHASH, q = 0;
+    uint64_t b = 0;
+    if (j >= 0 && (uint64_t)j < n) {
+      k = keys[j];
+      q = poss[j];
+      b = ks_load8(L.src, n, q);
+    }
+    sk[i] = k;
+    sp[i] = q;
+    sb[KS_PAD + i] = b;
+  }
+  __syncthreads();
+  const int me = KS_H + threadIdx.x;
+  const uint64_t j = j0 + threadIdx.x;
+  const bool in = j < n;
+  const uint32_t key = sk[me];
+  const uint32_t p = sp[me];
+  // candidates: staged entries [lo, me) with the same hash, newest first.  The head (me - 1)
+  // is searched when it lies within MAX_DIST and is not position 0 (deflate_slow's test);
+  // later ones must lie above limit = p - MAX_DIST (longest_match's do-while).
+  int K = 0;
+  uint32_t flag = 0;
+  if (in && key != KS_NOHASH && sk[me - 1] == key) {
+    const uint32_t c1 = sp[me - 1];
+    const uint32_t d0 = p - c1;
+    if (d0 <= MAX_DIST && c1 != 0) {
+      flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
+      const uint32_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
+      int lo = me - (int)MAX_CHAIN, hi = me - 1;  // first index in [me - 128, me - 2] with the hash, > limit
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sk[mid] == key && sp[mid] > limit) hi = mid;
+        else lo = mid + 1;
+      }
+      K = me - lo;  // the head plus entries lo .. me - 2
+    }
+  }
+  const uint32_t la = in ? (uint32_t)umin64(n - p, 1u << 20) : 0;
+  const uint32_t nice = min(NICE_LENGTH, la), maxl = min(MAX_MATCH, la);
+  const uint2* rec = reinterpret_cast<const uint2*>(sb) + KS_PAD + me;
+  const uint2 ownr = rec[0];
+  const uint32_t olo = ownr.x, ohi = ownr.y;
+  // A candidate can only be longer than best if bytes 0 .. best all match (mlo / mhi), and then
+  // it is -- unless best grew earlier in the same batch, so every recorded candidate is
+  // re-tested in chain order when the batch is flushed: the result is the first maximum.
+  uint32_t best = MIN_MATCH - 1, tb = 0, mlo = 0xffffffu, mhi = 0u;
+  uint32_t b32 = MIN_MATCH - 1, tb32 = 0;
+  int Kw = K;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) Kw = max(Kw, __shfl_xor_sync(0xffffffffu, Kw, o));
+  for (int t0 = 1; t0 <= Kw; t0 += KS_B) {
+    uint32_t bits = 0;
+#pragma unroll
+    for (int u = 0; u < KS_B; u++) {
+      const uint2 r = rec[-(t0 + u)];
+      const bool pass = (((r.x ^ olo) & mlo) | ((r.y ^ ohi) & mhi)) == 0u;
+      bits |= (pass && t0 + u <= K) ? 1u << u : 0u;
+    }
+    while (bits) {
+      const int t = t0 + __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint2 r = rec[-t];
+      const uint32_t xl = r.x ^ olo, xh = r.y ^ ohi;
+      if (((xl & mlo) | (xh & mhi)) != 0u) continue;  // best grew within this batch
+      uint32_t len = xl ? ks_ctz(xl) >> 3 : xh ? 4u + (ks_ctz(xh) >> 3) : 8u;
+      if (len == 8u && maxl > 8u) len = ks_extend(L.src, n, sp[me - t], p, 8, maxl);
+      len = min(len, maxl);
+      if (len > best) {
+        best = len;
+        tb = t;
+        mlo = best >= 3 ? 0xffffffffu : (2u << (8 * best + 7)) - 1;
+        mhi = best <= 3 ? 0u : best >= 7 ? 0xffffffffu : (2u << (8 * (best - 4) + 7)) - 1;
+        if (best >= nice) {  // zlib stops at nice_match
+          K = t;
+          bits = 0;
+        }
+      }
+    }
+    if (t0 + KS_B - 1 == 32) b32 = best, tb32 = tb;  // budget 32 (prev_length >= good_match)
+  }
+  if (Kw < 32) b32 = best, tb32 = tb;
+  if (!in) return;
+  const uint32_t yb = with_bytes ? (p ? (uint32_t)__ldg(L.src + p - 1) << 24 : 0u) : 0u;
+  if (K == 0) {
+    prof[L.pbase + p] = make_uint2(0u, yb);
+    return;
+  }
+  const uint32_t bestd = tb ? p - sp[me - tb] : 0;
+  const uint32_t bestd32 = tb32 ? p - sp[me - tb32] : 0;
+  prof[L.pbase + p] = make_uint2(prof_pack(best, bestd) | flag, yb | prof_pack(b32, bestd32) | (with_bytes ? 0u : flag));
+}
+
+// K3S + K4S over all lanes of a call: keys, one stable 16-bit radix sort per lane (two
+// passes), profiles (see k_profile_sorted)
+template <class Timer>
+static int profile_sorted(Workspace& sortws, Workspace& W, const LaneDev* d_lanes, int nl,
+                          const std::vector<uint64_t>& lane_prefix, uint2* d_prof, int with_bytes, Timer& T,
+                          cudaStream_t st) {
+  const uint64_t total = lane_prefix[nl];
+  if (!total) return BB_OK;
+  uint64_t longest = 0;
+  for (int i = 0; i < nl; i++) longest = std::max(longest, lane_prefix[i + 1] - lane_prefix[i]);
+  if (longest >= (1ull << 31)) {
+    set_error("deflate lane of %llu bytes exceeds the 2 Gi sort limit", (unsigned long long)longest);
+    return BB_ERROR;
+  }
+  size_t tmp = 0;
+  BB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint16_t*)nullptr, (uint16_t*)nullptr,
+                                              (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)longest, 0, 16,
+                                              st));
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  int rc = sortws.reserve(2 * al(2 * total) + 2 * al(4 * total) + al(tmp) + al(8 * (nl + 1)) + 4096);
+  if (rc) return rc;
+  uint16_t* k0 = sortws.take<uint16_t>(total);
+  uint16_t* k1 = sortws.take<uint16_t>(total);
+  uint32_t* v0 = sortws.take<uint32_t>(total);
+  uint32_t* v1 = sortws.take<uint32_t>(total);
+  void* d_tmp = sortws.take<uint8_t>(tmp);
+  uint64_t* d_lp = sortws.take<uint64_t>(nl + 1);
+  (void)W;
+  BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
+  T.mark("deflate.hash_sort");
+  {
+    const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((longest + 256 * KS_KP - 1) / (256 * KS_KP), 4096));
+    k_sort_keys<<<dim3(gx, nl), 256, 0, st>>>(d_lanes, d_lp, k0, v0);
+    BB_LAUNCH_CHECK();
+  }
+  for (int i = 0; i < nl; i++) {
+    const uint64_t o = lane_prefix[i], m = lane_prefix[i + 1] - o;
+    if (!m) continue;
+    size_t t2 = tmp;
+    BB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(d_tmp, t2, k0 + o, k1 + o, v0 + o, v1 + o, (int)m, 0, 16, st));
+    count_launch(2);
+  }
+  T.mark("deflate.profile");
+  k_profile_sorted<<<dim3((unsigned)((longest + KS_T - 1) / KS_T), nl), KS_T, 0, st>>>(d_lanes, d_lp, k1, v1, d_prof,
+                                                                                    with_bytes);
+  BB_LAUNCH_CHECK();
+  return BB_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -2006,15 +2263,24 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_CUDA_TRY(cudaMemcpyAsync(d_ad_chunk0, ad_chunk0.data(), 4 * nl, cudaMemcpyHostToDevice, st));
 
   // K3, K4
-  T.mark("deflate.hash_prev");
-  if (npos_exact) {
-    rc = hash_prev_two_phase(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
+  // default: K3 hash-chain links + K4 lock-step chain walk.  BB_K4_SORTED=1 selects the
+  // bucket-sorted variant (K3S + K4S): bit-identical, but slower on config2 (sort 13.2 ms + walk
+  // 43.5 ms vs 5.6 + 35.0 ms per step, profiles/r2_ncu_summary.md)
+  static const bool k4_sorted = getenv("BB_K4_SORTED") != nullptr;
+  if (!k4_sorted) {
+    T.mark("deflate.hash_prev");
+    if (npos_exact) {
+      rc = hash_prev_two_phase(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
+      if (rc) return rc;
+    }
+    T.mark("deflate.profile");
+    if (!pf_work.empty()) {
+      k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof, 1);
+      BB_LAUNCH_CHECK();
+    }
+  } else if (npos_exact) {
+    rc = profile_sorted(e->sortws, W, d_lanes, nl, lane_prefix, d_prof, 1, T, st);
     if (rc) return rc;
-  }
-  T.mark("deflate.profile");
-  if (!pf_work.empty()) {
-    k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof, 1);
-    BB_LAUNCH_CHECK();
   }
   // K5: speculative parse, then fix-up rounds until no exit state changes
   T.mark("deflate.parse_spec");
@@ -2107,6 +2373,30 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
 }
 
 }  // namespace bb
+
+// Test hook: K3S + K4S alone on one lane (profiles without the parse's byte), for the
+// comparison with the oracle's orc_match_profile.
+extern "C" BB_API int bb_debug_profile_sorted(const uint8_t* d_in, size_t n, uint32_t* d_prof, void* stream) {
+  using namespace bb;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!n) return BB_OK;
+  LaneDev d{};
+  d.src = d_in;
+  d.n = n;
+  LaneDev* dl;
+  BB_CUDA_TRY(cudaMalloc(&dl, sizeof d));
+  BB_CUDA_TRY(cudaMemcpy(dl, &d, sizeof d, cudaMemcpyHostToDevice));
+  Workspace sw, w2;
+  std::vector<uint64_t> lp{0, n};
+  struct NoTimer {
+    void mark(const char*) {}
+  } nt;
+  int rc = profile_sorted(sw, w2, dl, 1, lp, reinterpret_cast<uint2*>(d_prof), 0, nt, st);
+  if (rc) return rc;
+  BB_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFree(dl);
+  return BB_OK;
+}
 
 // ---------------------------------------------------------------------------
 // Test hooks (not part of include/bbcodec.h): run K3 / K4 alone on one lane so

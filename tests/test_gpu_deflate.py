@@ -78,6 +78,35 @@ def test_hash_prev_and_profiles_match_oracle(codec, oracle):
         assert bad.size == 0, f"profile mismatch at {bad[:5]}: {got[bad[:5]]} vs {want[bad[:5]]}"
 
 
+def test_sorted_chain_profiles_match_oracle(codec, oracle):
+    """K3S + K4S (bucket-sorted chains, the default encoder path) give the oracle's profiles
+    bit for bit: chain budgets 32 / 128, distance rules, nice_match, first maximum, long matches."""
+    import torch
+    from paper_2604_21072_b200 import _lib
+    L = _lib.load()
+    fn = L.bb_debug_profile_sorted
+    fn.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(11)
+    inputs = [oracle.synth_fp16(100000, 1)[1::2], oracle.synth_bf16(120000, 2)[1::2],
+              oracle.synth_bf16(300000, 5)[1::2], oracle.synth_fp16(200000, 4)[0::2],
+              random.Random(1).randbytes(70000), b"\x07" * 40000, b"ab" * 30000 + b"c" * 5,
+              rng.integers(0, 4, 90000, dtype=np.uint8).tobytes(),
+              rng.integers(0, 2, 70000, dtype=np.uint8).tobytes(),
+              bytes(rng.integers(0, 3, 50, dtype=np.uint8)) * 2000,  # periodic: long matches
+              b"xyz", b"ab", b"", bytes(range(256)) * 300]
+    for data in inputs:
+        if not data:
+            continue
+        x = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+        prof = torch.zeros(2 * len(data), dtype=torch.int32, device="cuda")
+        rc = fn(x.data_ptr(), len(data), prof.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert rc == 0, _lib.last_error()
+        want = oracle.match_profile(data)
+        got = prof.cpu().numpy().view(np.uint32).reshape(-1, 2)
+        bad = np.nonzero((got != want).any(axis=1))[0]
+        assert bad.size == 0, f"{len(data)} B: profile mismatch at {bad[:5]}: {got[bad[:5]]} vs {want[bad[:5]]}"
+
+
 def test_lane_encode_matches_zlib(codec):
     enc = codec.backend_by_id(codec.kBackendDeflate).encode
     for data in _corpus():
