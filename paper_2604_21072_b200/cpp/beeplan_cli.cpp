@@ -88,7 +88,7 @@ Args parse_args(int argc, char** argv) {
   static const std::set<std::string> kValued = {"--seed",   "--output",        "--format", "--backend",
                                                 "--role",   "--listen",        "--connect", "--shape",
                                                 "--payload", "--micro-batches", "--steps",  "--compute-ms",
-                                                "--stages", "--devices", "--placement"};
+                                                "--stages", "--devices", "--placement", "--reports"};
   static const std::set<std::string> kFlags = {"--no-split", "--compress"};
   Args a;
   for (int i = 1; i < argc; i++) {
@@ -226,6 +226,14 @@ int dispatch(const Args& a) {
         p["hop_bytes"] = where.hop_bytes;
         p["hop_peer"] = where.hop_peer;
         std::ofstream(a.opt.at("--placement")) << p.dump(2) << "\n";
+      }
+      if (a.opt.count("--reports")) {  // every role's records (wire_report_to_json), for diagnosis
+        J all;
+        all["source"] = J::parse(beeplan::wire_report_to_json(r.source));
+        all["stages"] = J::array();
+        for (const auto& st : r.stages) all["stages"].push_back(J::parse(beeplan::wire_report_to_json(st)));
+        all["sink"] = J::parse(beeplan::wire_report_to_json(r.sink));
+        std::ofstream(a.opt.at("--reports")) << all.dump(1) << "\n";
       }
       write_output(output, beeplan::wire_local_result_to_json(r));
       return r.sink.payload_ok ? 0 : 1;

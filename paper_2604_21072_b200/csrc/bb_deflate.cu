@@ -670,9 +670,19 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
         // candidate is walked but never recorded: chains only go backwards
         uint32_t wc, we;  // the candidate's word; bytes (best - 1, best) of the candidate
         asm("ld.shared.u32 %0, [%1];" : "=r"(wc) : "r"(sw + ic4));
+#ifdef PF_COND_LD2
+        // variant: the scan_end pair fetched only for candidates whose bytes 0, 1 match (hash
+        // collisions and dead lanes issue no second load).  Measured slower: 39.7 vs 35.0 ms
+        asm("{\n\t.reg .pred q;\n\tsetp.eq.u32 q, %2, %3;\n\tmov.u32 %0, 0xffffffff;\n\t"
+            "@q ld.shared.u16 %0, [%1];\n\t}"
+            : "=r"(we) : "r"(ic4 + offb), "r"(wc >> 16), "r"(key & 0xffffu));
+        cand[t] = ic4;
+        mask |= ((we == key >> 16) && (wc >> 16) == (key & 0xffffu) && ic4 > lim4) ? 1u << t : 0u;
+#else
         asm("ld.shared.u16 %0, [%1];" : "=r"(we) : "r"(ic4 + offb));
         cand[t] = ic4;
         mask |= (__byte_perm(wc, we, 0x5432) == key && ic4 > lim4) ? 1u << t : 0u;
+#endif
         ic4 = (wc << 2) & 0x3fffc;
       }
       if (__any_sync(0xffffffffu, mask != 0)) {
@@ -1510,7 +1520,11 @@ constexpr int BK_THREADS = 32;  // one warp per block: measured 3.1 ms vs 4.8 ms
 constexpr int BK_THREADS = BK_THREADS_OVR;
 #endif
 
-__global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict__ lanes,
+// NT threads per block: one warp when blocks are plentiful (register-limited occupancy);
+// 256 threads with per-warp histograms when a call has few blocks (small lanes: the
+// histogram of a block's 16383 symbols is then the latency of the whole stage)
+template <int NT>
+__global__ void __launch_bounds__(NT) k_blocks(const LaneDev* __restrict__ lanes,
                                                        const uint32_t* __restrict__ blk_lane,
                                                        uint32_t nblk_slots, const LaneSyms* __restrict__ ls,
                                                        const uint32_t* __restrict__ syms,
@@ -1521,9 +1535,12 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   __shared__ uint32_t hw_buf[HDR_BYTES / 4];
   __shared__ uint32_t s_len_sum, s_last_len, s_hdr_bits;
   // symbol counts as packed u16 pairs (a block has <= 16383 symbols)
-  __shared__ uint32_t h_l2[(L_CODES + 1) / 2], h_d2[(D_CODES + 1) / 2];
-  auto h_l = [&](int i) -> uint32_t { return (h_l2[i >> 1] >> (16 * (i & 1))) & 0xffff; };
-  auto h_d = [&](int i) -> uint32_t { return (h_d2[i >> 1] >> (16 * (i & 1))) & 0xffff; };
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t h_l2w[NW][(L_CODES + 1) / 2], h_d2w[NW][(D_CODES + 1) / 2];
+  uint32_t* h_l2 = h_l2w[threadIdx.x >> 5];  // this warp's histogram (merged into warp 0's below)
+  uint32_t* h_d2 = h_d2w[threadIdx.x >> 5];
+  auto h_l = [&](int i) -> uint32_t { return (h_l2w[0][i >> 1] >> (16 * (i & 1))) & 0xffff; };
+  auto h_d = [&](int i) -> uint32_t { return (h_d2w[0][i >> 1] >> (16 * (i & 1))) & 0xffff; };
   uint32_t slot = blockIdx.x;
   if (slot >= nblk_slots) return;
   const uint32_t li = blk_lane[slot];
@@ -1539,8 +1556,8 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   const uint32_t nsym = (uint32_t)(s1 - s0);
   // init (init_block: END_BLOCK freq 1)
   for (int i = threadIdx.x; i < (int)BL_CODES; i += blockDim.x) S.blt.freq[i] = 0;
-  for (int i = threadIdx.x; i < (int)(L_CODES + 1) / 2; i += blockDim.x) h_l2[i] = 0;
-  for (int i = threadIdx.x; i < (int)(D_CODES + 1) / 2; i += blockDim.x) h_d2[i] = 0;
+  for (int i = threadIdx.x; i < NW * (int)(L_CODES + 1) / 2; i += blockDim.x) (&h_l2w[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < NW * (int)(D_CODES + 1) / 2; i += blockDim.x) (&h_d2w[0][0])[i] = 0;
   for (int i = threadIdx.x; i < (int)(HDR_BYTES / 4); i += blockDim.x) hw_buf[i] = 0;
   if (threadIdx.x == 0) {
     s_len_sum = 0;
@@ -1565,18 +1582,31 @@ __global__ void __launch_bounds__(BK_THREADS) k_blocks(const LaneDev* __restrict
   {
     // four independent loads in flight per thread (the symbol stream comes from DRAM)
     uint32_t i = threadIdx.x;
-    for (; i + 3 * BK_THREADS < nsym; i += 4 * BK_THREADS) {
-      const uint32_t v0 = __ldg(sy + i), v1 = __ldg(sy + i + BK_THREADS), v2 = __ldg(sy + i + 2 * BK_THREADS),
-                     v3 = __ldg(sy + i + 3 * BK_THREADS);
+    for (; i + 3 * NT < nsym; i += 4 * NT) {
+      const uint32_t v0 = __ldg(sy + i), v1 = __ldg(sy + i + NT), v2 = __ldg(sy + i + 2 * NT),
+                     v3 = __ldg(sy + i + 3 * NT);
       count(v0), count(v1), count(v2), count(v3);
     }
-    for (; i < nsym; i += BK_THREADS) count(__ldg(sy + i));
+    for (; i < nsym; i += NT) count(__ldg(sy + i));
     if (threadIdx.x == 0 && nsym) s_last_len = sym_len(__ldg(sy + nsym - 1));
   }
   // reduce stored length
   for (int o = 16; o; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(&s_len_sum, local);
   __syncthreads();
+  if (NW > 1) {  // merge the per-warp counts (packed u16 pairs: a block has <= 16383 symbols)
+    for (int i = threadIdx.x; i < (int)(L_CODES + 1) / 2; i += blockDim.x) {
+      uint32_t v = 0;
+      for (int w = 1; w < NW; w++) v += h_l2w[w][i];
+      h_l2w[0][i] += v;
+    }
+    for (int i = threadIdx.x; i < (int)(D_CODES + 1) / 2; i += blockDim.x) {
+      uint32_t v = 0;
+      for (int w = 1; w < NW; w++) v += h_d2w[w][i];
+      h_d2w[0][i] += v;
+    }
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) S.lt.freq[i] = (uint16_t)(h_l(i) + (i == 256));
   for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) S.dt.freq[i] = (uint16_t)h_d(i);
   __syncthreads();
@@ -2332,7 +2362,11 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_LAUNCH_CHECK();
   T.mark("deflate.blocks_trees");
   BB_CUDA_TRY(cudaMemsetAsync(d_hdr, 0, (size_t)blk_total * HDR_BYTES, st));
-  k_blocks<<<blk_total, BK_THREADS, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_syms, d_info, d_codes, d_hdr);
+  if (blk_total < 4u * kNumSMs)
+    k_blocks<256><<<blk_total, 256, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_syms, d_info, d_codes, d_hdr);
+  else
+    k_blocks<BK_THREADS><<<blk_total, BK_THREADS, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_syms, d_info,
+                                                           d_codes, d_hdr);
   BB_LAUNCH_CHECK();
   T.mark("deflate.layout_zero");
   k_layout<<<(nl + 3) / 4, 128, 0, st>>>(d_lanes, nl, d_ls, d_info, d_plan, d_blob_len);
