@@ -116,4 +116,35 @@ __device__ __forceinline__ void gather8(const uint8_t* q, uint32_t out[2]) {
   out[1] = __funnelshift_r(j ? w[2] : w[1], j ? w[3] : w[2], r);
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, sm_90+): one elected thread moves a 16-byte
+// aligned tile global -> shared through the copy engine, completion tracked by a
+// shared-memory mbarrier (transaction bytes).  Used to stage tiles whose bytes
+// are then expanded by the CTA (inflate's LZ77 resolution windows).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arm the barrier for `bytes` and start the copy (one thread; sizes and addresses 16-byte aligned)
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 }  // namespace bb

@@ -1512,26 +1512,34 @@ constexpr uint32_t RESOLVED = 0x80000000u;
 #define RS_THREADS_OVR 1024
 #endif
 constexpr int RS_THREADS = RS_THREADS_OVR;
+constexpr uint32_t RS_SMEM = SUB * 4 + SUB;  // window entries + the TMA-staged raw bytes
 
 struct ExtEntry {
   uint32_t dst;
   uint32_t src;
 };
 
-// window entries <- RESOLVED | byte, 16 bytes per 128-bit load where aligned
-__device__ __forceinline__ void fill_entries(uint32_t* ent, const uint8_t* src, uint32_t w, uint32_t total) {
-  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-    const uint32_t nv = w / 16;
-    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
-      const uint4 x = __ldg(reinterpret_cast<const uint4*>(src) + v);
-      const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int k = 0; k < 16; k++) ent[16 * v + k] = RESOLVED | ((wd[k >> 2] >> (8 * (k & 3))) & 0xff);
-    }
-    for (uint32_t i = 16 * nv + threadIdx.x; i < total; i += blockDim.x) ent[i] = RESOLVED | (i < w ? src[i] : 0u);
-  } else {
-    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) ent[i] = RESOLVED | (i < w ? src[i] : 0u);
+// window entries <- RESOLVED | byte.  The window's bytes (already written literals and
+// stored runs) are staged into shared memory by a TMA bulk copy (16-byte aligned part) and
+// expanded from there 16 at a time; `raw` holds SUB bytes behind the SUB entries.
+__device__ __forceinline__ void fill_entries(uint32_t* ent, uint8_t* raw, uint64_t* bar, const uint8_t* src,
+                                             uint32_t w, uint32_t total) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  const uint32_t wa = aligned ? (w & ~15u) : 0u;  // bytes moved by the copy engine
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    if (wa) tma_load_1d(raw, src, wa, bar);
   }
+  __syncthreads();
+  if (wa) mbar_wait(bar, 0);
+  const uint4* r4 = reinterpret_cast<const uint4*>(raw);
+  for (uint32_t v = threadIdx.x; v < wa / 16; v += blockDim.x) {
+    const uint4 x = r4[v];
+    const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 16; k++) ent[16 * v + k] = RESOLVED | ((wd[k >> 2] >> (8 * (k & 3))) & 0xff);
+  }
+  for (uint32_t i = wa + threadIdx.x; i < total; i += blockDim.x) ent[i] = RESOLVED | (i < w ? src[i] : 0u);
 }
 
 __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __restrict__ jobs,
@@ -1545,6 +1553,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
                                                               uint8_t* __restrict__ wflag) {
   extern __shared__ uint32_t ent[];  // SUB entries: RESOLVED | value, or source relative to S - 65536
   __shared__ int changed;
+  __shared__ __align__(8) uint64_t s_bar;  // TMA completion of the window's bytes
   __shared__ uint32_t s_cnt;
   const uint32_t j = job_of_sub[blockIdx.x];
   const PJob J = jobs[j];
@@ -1566,7 +1575,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_resolve_local(const PJob* __rest
     return;
   }
   if (threadIdx.x == 0) wflag[blockIdx.x] = 1;
-  fill_entries(ent, J.dst + S, W, W);
+  fill_entries(ent, reinterpret_cast<uint8_t*>(ent + SUB), &s_bar, J.dst + S, W, W);
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   __shared__ int corrupt;
@@ -1639,6 +1648,7 @@ __global__ void __cluster_dims__(RS_CL, 1, 1) __launch_bounds__(RS_THREADS)
                       uint32_t* __restrict__ extp, uint8_t* __restrict__ wflag) {
   extern __shared__ uint32_t ent[];
   __shared__ int s_corrupt, s_anyv[3];
+  __shared__ __align__(8) uint64_t s_bar;  // TMA completion of the window's bytes
   __shared__ uint32_t s_cnt;
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
@@ -1675,7 +1685,7 @@ __global__ void __cluster_dims__(RS_CL, 1, 1) __launch_bounds__(RS_THREADS)
     cl.sync();  // rank 0's flag is read by all before anyone exits
     return;
   }
-  fill_entries(ent, J.dst + S, Wn, SUB);
+  fill_entries(ent, reinterpret_cast<uint8_t*>(ent + SUB), &s_bar, J.dst + S, Wn, SUB);
   __syncthreads();
   if (has_m) {
     for (uint64_t k = m0 + threadIdx.x; k < nm && M[k].dst < S + Wn; k += blockDim.x) {
@@ -1985,8 +1995,8 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     std::lock_guard<std::mutex> attr_lock(attr_mu);
     if (!attr_done[dev]) {
       BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
-      BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
-      BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB * 4));
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_SMEM));
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_SMEM));
       BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(WarpSm) * WD_WARPS)));
       attr_done[dev] = true;
@@ -2262,14 +2272,14 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     // the dynamic pass (B) resolves copy chains over clusters of windows
     static const bool single = getenv("BB_RESOLVE_SINGLE") != nullptr;
     if (single || !find_dynamic) {
-      k_resolve_local<<<(unsigned)sub_job.size(), RS_THREADS, SUB * 4, st>>>(d_jobs, d_sub_job, d_out_total, d_fail,
+      k_resolve_local<<<(unsigned)sub_job.size(), RS_THREADS, RS_SMEM, st>>>(d_jobs, d_sub_job, d_out_total, d_fail,
                                                                        d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
     } else {
       std::vector<uint2> clm;
       for (int i = 0; i < nj; i++)
         for (uint32_t w0 = 0; w0 < J[i].nsub; w0 += RS_CL) clm.push_back(make_uint2((uint32_t)i, w0));
       BB_CUDA_TRY(cudaMemcpyAsync(d_clm, clm.data(), sizeof(uint2) * clm.size(), cudaMemcpyHostToDevice, st));
-      k_resolve_cluster<<<(unsigned)(clm.size() * RS_CL), RS_THREADS, SUB * 4, st>>>(
+      k_resolve_cluster<<<(unsigned)(clm.size() * RS_CL), RS_THREADS, RS_SMEM, st>>>(
           d_jobs, d_clm, d_out_total, d_fail, d_matches, d_ext, d_ext_cnt, d_extp, d_wflag);
     }
     BB_LAUNCH_CHECK();
