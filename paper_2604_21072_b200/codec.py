@@ -17,7 +17,9 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import struct
+import sys
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional, Sequence
 
@@ -70,8 +72,21 @@ def _check(rc: int) -> None:
         raise _STATUS.get(rc, Error)(_lib.last_error())
 
 
+def _device() -> int:
+    """The device of the module-level (host-buffer) calls: BEEPLAN_CUDA_DEVICE, else the caller's
+    current torch device when torch has initialised CUDA (a torchrun worker bound to GPU k stays on
+    GPU k), else 0 -- the C++ drop-in's rule (cpp/codec.cpp)."""
+    env = os.environ.get("BEEPLAN_CUDA_DEVICE")
+    if env:
+        return int(env)
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        return torch.cuda.current_device()
+    return 0
+
+
 def _ctx():
-    return _lib.context(0)
+    return _lib.context(_device())
 
 
 def _out(n: int):

@@ -454,10 +454,14 @@ class RoleDevice {
     codec_ok(bb_ctx_create(&ctx_, dev));
     WIRE_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     WIRE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pinned_), 64, cudaHostAllocDefault));
+    // waits of the pacing threads yield the CPU instead of spinning: a box runs 3 threads per role,
+    // and a spinning waiter delays the token bucket's wake-ups (link jitter)
+    WIRE_CUDA(cudaEventCreateWithFlags(&done_, cudaEventBlockingSync | cudaEventDisableTiming));
   }
   ~RoleDevice() {
     cudaSetDevice(dev_);
     if (st_) cudaStreamSynchronize(st_);
+    if (done_) cudaEventDestroy(done_);
     if (pinned_) cudaFreeHost(pinned_);
     if (st_) cudaStreamDestroy(st_);
     bb_ctx_destroy(ctx_);
@@ -468,12 +472,16 @@ class RoleDevice {
   bb_ctx* ctx() const { return ctx_; }
   cudaStream_t stream() const { return st_; }
   std::uint8_t* pinned() const { return pinned_; }
-  void sync() { WIRE_CUDA(cudaStreamSynchronize(st_)); }
+  void sync() {
+    WIRE_CUDA(cudaEventRecord(done_, st_));
+    WIRE_CUDA(cudaEventSynchronize(done_));
+  }
 
  private:
   int dev_;
   bb_ctx* ctx_ = nullptr;
   cudaStream_t st_ = nullptr;
+  cudaEvent_t done_ = nullptr;
   std::uint8_t* pinned_ = nullptr;
 };
 

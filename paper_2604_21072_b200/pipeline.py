@@ -357,7 +357,9 @@ def run_pipeline(args) -> dict:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime  # a failed stage must not block its neighbours forever (NCCL watchdog)
+        dist.init_process_group("nccl", device_id=dev,
+                                timeout=datetime.timedelta(seconds=int(os.environ.get("BB_NCCL_TIMEOUT_S", "600"))))
     rank = dist.get_rank() if world > 1 else 0
     dc = codec.DeviceCodec(local)
     spans = step_spans(args.payload, args.micro_batches)
