@@ -454,9 +454,7 @@ class RoleDevice {
     codec_ok(bb_ctx_create(&ctx_, dev));
     WIRE_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     WIRE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pinned_), 64, cudaHostAllocDefault));
-    // waits of the pacing threads yield the CPU instead of spinning: a box runs 3 threads per role,
-    // and a spinning waiter delays the token bucket's wake-ups (link jitter)
-    WIRE_CUDA(cudaEventCreateWithFlags(&done_, cudaEventBlockingSync | cudaEventDisableTiming));
+    WIRE_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
   }
   ~RoleDevice() {
     cudaSetDevice(dev_);
@@ -472,9 +470,19 @@ class RoleDevice {
   bb_ctx* ctx() const { return ctx_; }
   cudaStream_t stream() const { return st_; }
   std::uint8_t* pinned() const { return pinned_; }
+  // waits of the pacing threads poll briefly, then sleep between polls instead of spinning: a box
+  // runs three threads per role, and spinning waiters delay the token buckets' wake-ups (link
+  // jitter).  (A cudaEventBlockingSync wait measured ~25 ms of wake-up latency per frame.)
   void sync() {
     WIRE_CUDA(cudaEventRecord(done_, st_));
-    WIRE_CUDA(cudaEventSynchronize(done_));
+    const auto t0 = Clock::now();
+    for (;;) {
+      const cudaError_t e = cudaEventQuery(done_);
+      if (e == cudaSuccess) return;
+      if (e != cudaErrorNotReady) cuda_fail(e, "cudaEventQuery");
+      if (Clock::now() - t0 < std::chrono::microseconds(100)) std::this_thread::yield();
+      else std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
   }
 
  private:
