@@ -57,12 +57,28 @@ def main():
     ap.add_argument("--rates", default="100")
     ap.add_argument("--micro", default="1,8")
     ap.add_argument("--hidden", type=int, default=8192)
+    ap.add_argument("--sizes-mib", default="",
+                    help="config5 sweep: payload sizes (MiB, d=8192 fp16 rows), run at --micro[0] compressed "
+                         "and uncompressed, one step each")
     args = ap.parse_args()
     import torch
     g = torch.cuda.device_count()
     devices = ",".join(str(d) for d in range(g))
     stages = max(0, g - 2)  # source + stages + sink = one role per GPU
     res = {"gpus": g, "devices": devices, "stages": stages, "runs": []}
+    if args.sizes_mib:
+        micro = int(args.micro.split(",")[-1])
+        for mib in [int(x) for x in args.sizes_mib.split(",")]:
+            for compress in (False, True):
+                r = run(mib << 20, micro, 1, stages, float(args.rates.split(",")[0]), compress, devices)
+                if "end_to_end_ms" in r:
+                    r["pipelined_rows_per_s"] = r["payload_bytes"] / 2 / args.hidden / (r["end_to_end_ms"] / 1e3)
+                res["runs"].append(r)
+                print(json.dumps({k: r.get(k) for k in ("payload_bytes", "compress", "end_to_end_ms", "payload_ok",
+                                                        "error")}), flush=True)
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+        return 0
     for rate in [float(x) for x in args.rates.split(",")]:
         for micro in [int(x) for x in args.micro.split(",")]:
             for compress in (False, True):
