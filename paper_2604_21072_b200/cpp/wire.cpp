@@ -203,6 +203,41 @@ class FirstFailure {
   std::exception_ptr first_;
 };
 
+// every role's device context is created and its codec warmed up before the source's first
+// offer (the clock of end_to_end_ms): module loading and workspace growth are setup, not transfer
+class Latch {
+ public:
+  explicit Latch(int n) : n_(n) {}
+  void arrive() {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (--n_ <= 0) cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return n_ <= 0; });
+  }
+
+ private:
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int n_;
+};
+
+// arrives at the latch once: when the role is ready, or when it unwinds before that
+class Arrival {
+ public:
+  explicit Arrival(Latch& l) : l_(l) {}
+  ~Arrival() { now(); }
+  void now() {
+    if (!done_) l_.arrive();
+    done_ = true;
+  }
+
+ private:
+  Latch& l_;
+  bool done_ = false;
+};
+
 // make_step_slices' spans (wire.cpp:321-336): elements split into M spans, the
 // first `rem` spans one element longer
 std::vector<std::pair<std::size_t, std::size_t>> step_spans(std::size_t payload_bytes, int micro) {
@@ -696,6 +731,23 @@ std::size_t container_decoded_size(RoleDevice& rd, const std::uint8_t* c, std::s
   return need;
 }
 
+// one compress + decompress of a buffer of `bytes` on the role's context: loads the codec's kernels
+// on this device and grows the context's workspaces to the run's frame size
+void warm_codec(RoleDevice& rd, std::size_t bytes, std::uint8_t backend) {
+  if (bytes < 2) return;
+  bytes &= ~std::size_t(1);
+  DevBuf in, out, back;
+  const std::size_t cap = bb_compress_bound(bytes, backend, 1);
+  in.ensure(rd.dev(), bytes);
+  out.ensure(rd.dev(), cap);
+  back.ensure(rd.dev(), bytes);
+  WIRE_CUDA(cudaMemsetAsync(in.get(), 0x3c, bytes, rd.stream()));
+  std::size_t len = 0, got = 0;
+  codec_ok(bb_compress(rd.ctx(), in.get(), bytes, backend, 1, out.get(), cap, &len, rd.stream()));
+  codec_ok(bb_decompress(rd.ctx(), out.get(), len, back.get(), bytes, &got, rd.stream()));
+  rd.sync();
+}
+
 std::vector<int> wire_devices(const std::vector<int>& asked) {
   if (!asked.empty()) return asked;
   std::vector<int> devs;
@@ -1002,6 +1054,10 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     failure.record(std::current_exception());
     close_role(r);
   };
+  // source, sink, and per stage its compute worker warm up; recv / send workers only create contexts
+  Latch ready(2 + cfg.stage_count);
+  std::size_t warm_bytes = 0;
+  for (const auto& sp : spans) warm_bytes = std::max(warm_bytes, sp.second);
   const std::uint8_t backend = cfg.backend;
   const std::size_t frame_cap = [&] {
     std::size_t mx = 0;
@@ -1014,7 +1070,10 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
   threads.emplace_back([&] {
     const int r = roles - 1;
     try {
+      Arrival arrival(ready);
       RoleDevice rd(sink_dev);
+      if (cfg.compress) warm_codec(rd, warm_bytes, cfg.backend);
+      arrival.now();
       Inbox& in = *inbox.back();
       WireRoleReport& rep = result.sink;
       DevBuf assembled;
@@ -1135,7 +1194,10 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
       });
       std::thread work([&] {
         try {
+          Arrival arrival(ready);
           RoleDevice rd(dev);
+          if (cfg.compress) warm_codec(rd, warm_bytes, cfg.backend);
+          arrival.now();
           for (;;) {
             DevFrame f = inbound.pop().value_or(shutdown());
             if (f.head.type == WireFrame::Type::Shutdown) {
@@ -1233,6 +1295,9 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     const int r = 0;
     try {
       RoleDevice rd(src_dev);
+      if (cfg.compress) warm_codec(rd, warm_bytes, cfg.backend);
+      ready.arrive();
+      ready.wait();  // every role is up (or failed): the first offer starts end_to_end_ms
       HopSender& out = *hop.front();
       WireRoleReport& rep = result.source;
       DevBuf frame;

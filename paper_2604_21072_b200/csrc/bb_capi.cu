@@ -471,20 +471,22 @@ int bb_decompress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, cons
   cudaStream_t st = S(stream);
   std::vector<int> st_local(count > 0 ? count : 1);
   int* stv = status ? status : st_local.data();
-  // 1. headers to the host (parse_container runs host-side on 31 bytes)
-  std::vector<uint8_t> hdr((size_t)count * BB_CONTAINER_HEADER + 1);
+  // 1. headers to the host (parse_container runs host-side on 31 bytes), with the first bytes of the
+  //    high blob: its first block's BTYPE routes dynamic lanes straight to the full candidate search
+  constexpr size_t HB = BB_CONTAINER_HEADER + 3, HS = 40;  // bytes read / host stride per item
+  std::vector<uint8_t> hdr((size_t)count * HS + 1);
   for (int i = 0; i < count; i++) {
     out_len[i] = 0;
     if (n[i] >= BB_CONTAINER_HEADER)
-      BB_CUDA_TRY(cudaMemcpyAsync(hdr.data() + (size_t)i * BB_CONTAINER_HEADER, d_in[i],
-                                  BB_CONTAINER_HEADER, cudaMemcpyDeviceToHost, st));
+      BB_CUDA_TRY(cudaMemcpyAsync(hdr.data() + (size_t)i * HS, d_in[i], std::min<size_t>(n[i], HB),
+                                  cudaMemcpyDeviceToHost, st));
   }
   BB_CUDA_TRY(cudaStreamSynchronize(st));
   std::vector<Header> H(count > 0 ? count : 1);
   std::vector<uint64_t> dec(count > 0 ? count : 1, 0);
   size_t scratch = 0;
   for (int i = 0; i < count; i++) {
-    stv[i] = parse_header(hdr.data() + (size_t)i * BB_CONTAINER_HEADER, n[i], &H[i]);
+    stv[i] = parse_header(hdr.data() + (size_t)i * HS, n[i], &H[i]);
     if (!stv[i]) stv[i] = plan_decode(H[i], &dec[i]);
     if (!stv[i]) {
       out_len[i] = dec[i];
@@ -528,7 +530,9 @@ int bb_decompress_batch(bb_ctx* ctx, int count, const uint8_t* const* d_in, cons
     if (c.split) {
       uint8_t* hi = ctx->ws.take<uint8_t>(c.count + 16);
       uint8_t* lo = ctx->ws.take<uint8_t>(c.count + 16);
-      jobs.push_back(InflateJob{hb, c.hl, hi, c.count});
+      const uint8_t* h3 = hdr.data() + (size_t)i * HS + BB_CONTAINER_HEADER;  // zlib CMF, FLG, first block
+      const int bt = (c.hl >= 3 && n[i] >= HB) ? (h3[2] >> 1) & 3 : -1;
+      jobs.push_back(InflateJob{hb, c.hl, hi, c.count, bt});
       job_item.push_back(i);
       jobs.push_back(InflateJob{lb, c.ll, lo, c.count});
       job_item.push_back(i);

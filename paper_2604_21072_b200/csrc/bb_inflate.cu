@@ -395,10 +395,20 @@ int inflate_lanes(InflateEngine* e, const std::vector<InflateJob>& jobs, cudaStr
     }
   }
   if (!big.empty()) {
-    // pass A: stored-block chains only (cheap); pass B: full candidate search for the rest
-    std::vector<int> ok(big.size());
-    int rc = par_inflate(e->par, big, st, ok.data(), 0);
-    if (rc) return rc;
+    // pass A: stored-block chains only (cheap); pass B: full candidate search for the rest.  Lanes
+    // whose first block is known to be dynamic (the caller read its BTYPE) skip pass A.
+    std::vector<int> ok(big.size(), 0);
+    std::vector<InflateJob> pass_a;
+    std::vector<size_t> a_k;
+    for (size_t k = 0; k < big.size(); k++)
+      if (big[k].btype0 != 2) pass_a.push_back(big[k]), a_k.push_back(k);
+    if (!pass_a.empty()) {
+      std::vector<int> oka(pass_a.size());
+      int rc = par_inflate(e->par, pass_a, st, oka.data(), 0);
+      if (rc) return rc;
+      for (size_t q = 0; q < pass_a.size(); q++) ok[a_k[q]] = oka[q];
+    }
+    int rc = BB_OK;
     std::vector<InflateJob> dyn;
     std::vector<size_t> dyn_k;
     for (size_t k = 0; k < big.size(); k++)

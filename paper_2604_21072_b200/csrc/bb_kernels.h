@@ -76,6 +76,7 @@ struct InflateJob {
   uint64_t n;
   uint8_t* dst;
   uint64_t expected;
+  int btype0 = -1;  // BTYPE of the stream's first block when the caller read it (-1: unknown)
 };
 struct InflateEngine;
 InflateEngine* inflate_engine_create();

@@ -4,8 +4,15 @@
 // wire.cpp:441-450).  Built by tests/cpp/Makefile, run by tests/test_wire_gpu_runner.py.
 #include <doctest.h>
 
+#include <arpa/inet.h>
+#include <netinet/in.h>
+#include <sys/socket.h>
+#include <unistd.h>
+
 #include <chrono>
 #include <cstdio>
+#include <future>
+#include <string>
 
 #include "beeplan/errors.hpp"
 #include "beeplan/wire.hpp"
@@ -103,4 +110,60 @@ TEST_CASE("GPU runner: compression shortens a 100 Mbps hop on Gaussian activatio
 TEST_CASE("GPU runner: odd payloads and bad stage counts are ValidationError") {
   CHECK_THROWS_AS(run_wire_local(relay(1, 1, 1001, false)), ValidationError);
   CHECK_THROWS_AS(run_wire_local(relay(-1, 1, 1000, false)), ValidationError);
+}
+
+namespace {
+
+int bound_listener(std::string* endpoint) {
+  int fd = ::socket(AF_INET, SOCK_STREAM, 0);
+  sockaddr_in sin{};
+  sin.sin_family = AF_INET;
+  sin.sin_port = 0;
+  inet_pton(AF_INET, "127.0.0.1", &sin.sin_addr);
+  if (fd < 0 || ::bind(fd, reinterpret_cast<sockaddr*>(&sin), sizeof(sin)) != 0 || ::listen(fd, 4) != 0) return -1;
+  socklen_t len = sizeof(sin);
+  ::getsockname(fd, reinterpret_cast<sockaddr*>(&sin), &len);
+  *endpoint = "127.0.0.1:" + std::to_string(ntohs(sin.sin_port));
+  return fd;
+}
+
+}  // namespace
+
+TEST_CASE("TCP roles: source -> stage -> sink over loopback sockets, codec on the GPU, bit-exact") {
+  std::string stage_ep, sink_ep;
+  const int stage_fd = bound_listener(&stage_ep), sink_fd = bound_listener(&sink_ep);
+  REQUIRE(stage_fd >= 0);
+  REQUIRE(sink_fd >= 0);
+  WireSinkConfig sk;
+  sk.payload_bytes = 1 << 20;
+  sk.micro_batches = 4;
+  sk.seed = 3;
+  sk.listen_fd = sink_fd;
+  WireStageConfig sg;
+  sg.listen_fd = stage_fd;
+  sg.connect = sink_ep;
+  sg.compress_out = true;
+  sg.compute_ms = 1.0;
+  WireSourceConfig so;
+  so.connect = stage_ep;
+  so.steps = 2;
+  so.micro_batches = 4;
+  so.payload_bytes = 1 << 20;
+  so.seed = 3;
+  so.compress = true;
+  so.shape.rate_bps = 400e6;
+  auto sink = std::async(std::launch::async, [&] { return run_wire_sink(sk); });
+  auto stage = std::async(std::launch::async, [&] { return run_wire_stage(sg); });
+  auto source = std::async(std::launch::async, [&] { return run_wire_source(so); });
+  WireRoleReport src = source.get(), st = stage.get(), dst = sink.get();
+  CHECK(dst.payload_ok);
+  CHECK(dst.frames_seen == 8);
+  CHECK(st.frames_seen == 8);
+  CHECK(src.codec_ms_total > 0.0);
+  CHECK(st.codec_ms_total > 0.0);
+  const HopMetrics h0 = join_hop_metrics(src, st), h1 = join_hop_metrics(st, dst);
+  CHECK(h0.frames == 8);
+  CHECK(h1.frames == 8);
+  ::close(stage_fd);
+  ::close(sink_fd);
 }
