@@ -1012,9 +1012,14 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
   const int steps = std::max(0, cfg.steps);
   std::vector<Bytes> host_streams(static_cast<std::size_t>(steps));
   {
+    const int nt = std::max(1, std::min<int>(steps, (int)std::max(1u, std::thread::hardware_concurrency())));
+    std::atomic<int> next{0};
     std::vector<std::thread> gen;
-    for (int s = 0; s < steps; ++s)
-      gen.emplace_back([&, s] { host_streams[static_cast<std::size_t>(s)] = step_stream(cfg.payload_bytes, cfg.seed, s); });
+    for (int k = 0; k < nt; ++k)
+      gen.emplace_back([&] {
+        for (int s; (s = next.fetch_add(1)) < steps;)
+          host_streams[static_cast<std::size_t>(s)] = step_stream(cfg.payload_bytes, cfg.seed, s);
+      });
     for (auto& t : gen) t.join();
   }
   const int src_dev = role_dev.front(), sink_dev = role_dev.back();
