@@ -691,6 +691,20 @@ class HopSender {
   }
   std::uint64_t bytes() const { return bytes_; }
 
+  // one small copy into the receiver's HBM before the clock starts: the first peer copy between
+  // two GPUs of a process sets up the mapping (measured: up to ~150 ms), which is not transfer time
+  void warm(RoleDevice& rd) {
+    DevBuf scratch;
+    scratch.ensure(rd.dev(), 256);
+    const int s = to_.acquire(256);
+    cudaError_t e = to_.dev() == rd.dev()
+                        ? cudaMemcpyAsync(to_.slot(s), scratch.get(), 256, cudaMemcpyDeviceToDevice, rd.stream())
+                        : cudaMemcpyPeerAsync(to_.slot(s), to_.dev(), scratch.get(), rd.dev(), 256, rd.stream());
+    if (e == cudaSuccess) e = cudaStreamSynchronize(rd.stream());
+    to_.release(s);
+    if (e != cudaSuccess) cuda_fail(e, "hop warm-up copy");
+  }
+
  private:
   Inbox& to_;
   Pacer pacer_;
@@ -1059,8 +1073,8 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     failure.record(std::current_exception());
     close_role(r);
   };
-  // source, sink, and per stage its compute worker warm up; recv / send workers only create contexts
-  Latch ready(2 + cfg.stage_count);
+  // source, sink, and per stage its compute and send workers warm up (codec, first peer copy)
+  Latch ready(2 + 2 * cfg.stage_count);
   std::size_t warm_bytes = 0;
   for (const auto& sp : spans) warm_bytes = std::max(warm_bytes, sp.second);
   const std::uint8_t backend = cfg.backend;
@@ -1263,7 +1277,10 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
       });
       std::thread tx([&] {
         try {
+          Arrival arrival(ready);
           RoleDevice rd(dev);
+          out.warm(rd);
+          arrival.now();
           for (;;) {
             DevFrame f = outbound.pop().value_or(shutdown());
             const bool last = f.head.type == WireFrame::Type::Shutdown;
@@ -1301,6 +1318,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     try {
       RoleDevice rd(src_dev);
       if (cfg.compress) warm_codec(rd, warm_bytes, cfg.backend);
+      hop.front()->warm(rd);
       ready.arrive();
       ready.wait();  // every role is up (or failed): the first offer starts end_to_end_ms
       HopSender& out = *hop.front();

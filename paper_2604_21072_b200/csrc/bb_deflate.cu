@@ -1787,39 +1787,10 @@ __global__ void k_place(const ContainerDev* __restrict__ cons, int ncons, const 
   if (C.split == 1) lane_out[C.lane0 + 1] = ok ? C.dst + hdr + hl : nullptr;
 }
 
-__global__ void k_zero(const ContainerDev* __restrict__ cons, const uint64_t* __restrict__ con_len,
-                       const int* __restrict__ con_status) {
-  const int c = blockIdx.y;
-  if (con_status[c] != BB_OK) return;
-  uint8_t* d = cons[c].dst;
-  const uint64_t len = con_len[c];
-  uintptr_t a = reinterpret_cast<uintptr_t>(d);
-  uint64_t head = (16 - (a & 15)) & 15;
-  if (head > len) head = len;
-  uint64_t vecs = (len - head) / 16;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < vecs; i += (uint64_t)gridDim.x * blockDim.x)
-    reinterpret_cast<uint4*>(d + head)[i] = make_uint4(0, 0, 0, 0);
-  if (blockIdx.x == 0) {
-    for (uint64_t i = threadIdx.x; i < head; i += blockDim.x) d[i] = 0;
-    for (uint64_t i = head + 16 * vecs + threadIdx.x; i < len; i += blockDim.x) d[i] = 0;
-  }
-}
-
-// OR `len` (<= 57) bits of v into a bit stream at absolute bit position `bit`
-// relative to the 4-byte-aligned word pointer `w`.
-__device__ __forceinline__ void or_bits_global(uint32_t* w, uint64_t bit, uint64_t v, uint32_t len) {
-  if (!len) return;
-  uint64_t i = bit >> 5;
-  uint32_t o = (uint32_t)(bit & 31);
-  atomicOr(&w[i], (uint32_t)(v << o));
-  if (o + len > 32) atomicOr(&w[i + 1], (uint32_t)(v >> (32 - o)));
-  if (o + len > 64) atomicOr(&w[i + 2], (uint32_t)(v >> (64 - o)));
-}
-
 // ---------------------------------------------------------------------------
 // K7: bit packing.  One CTA per block; symbols in chunks of 2048 (8 per
 // thread): bit lengths -> block scan -> shared-memory staging with atomicOr ->
-// interior words stored, edge words OR'ed into global memory.
+// complete words stored; the block's shared edge words merged by k_edges.
 constexpr int EM_THREADS = 256, EM_PER = 8, EM_CHUNK = EM_THREADS * EM_PER;
 constexpr int EM_WORDS = (EM_CHUNK * 48) / 32 + 4;
 
@@ -1856,6 +1827,15 @@ __device__ __forceinline__ void sym_bits(uint32_t v, const uint32_t* lcodes, con
   }
 }
 
+// Global writes of K7 are plain 32-bit stores of words a block owns entirely.  The block's first
+// word (when it starts mid-word, it holds the previous block's tail) and its last word (when it
+// ends mid-word) are not stored: their block-owned bits go to edge[2 * slot + {0, 1}] as
+// (word index relative to the lane's word base, value), and k_edges ORs the contributions that
+// land on the same word and stores each word once.  Nothing is pre-zeroed and no global atomics
+// are issued, so when the container lives in the next GPU's HBM (fused hand-off) every container
+// byte crosses NVLink once.
+constexpr uint32_t EDGE_NONE = 0xffffffffu;
+
 __global__ void __launch_bounds__(EM_THREADS) k_emit(const LaneDev* __restrict__ lanes,
                                                      const uint32_t* __restrict__ blk_lane, uint32_t nblk_slots,
                                                      const LaneSyms* __restrict__ ls,
@@ -1864,11 +1844,14 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const LaneDev* __restrict__
                                                      const BlockCodes* __restrict__ codes,
                                                      const uint32_t* __restrict__ hdr,
                                                      const uint32_t* __restrict__ syms,
-                                                     uint8_t* const* __restrict__ lane_out) {
+                                                     uint8_t* const* __restrict__ lane_out,
+                                                     uint2* __restrict__ edge) {
   typedef cub::BlockScan<uint32_t, EM_THREADS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ uint32_t stage[EM_WORDS];
   __shared__ uint32_t s_l[L_CODES], s_d[D_CODES];
+  __shared__ uint32_t s_carry;  // the block's partial word left by the previous piece
+  __shared__ uint2 s_lo;        // the block's first-word contribution
   const uint32_t slot = blockIdx.x;
   if (slot >= nblk_slots) return;
   const uint32_t li = blk_lane[slot];
@@ -1883,41 +1866,52 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const LaneDev* __restrict__
   uintptr_t a = reinterpret_cast<uintptr_t>(out);
   uint32_t* wbase = reinterpret_cast<uint32_t*>(a & ~uintptr_t(3));
   const uint64_t bit0 = 8ull * (a & 3) + pl.bit_off;
-  if (threadIdx.x == 0) or_bits_global(wbase, bit0, (pl.type << 1) | pl.last, 3);
+  const uint64_t wf = bit0 >> 5;
+  const bool first_shared = (bit0 & 31) != 0;
+  const uint32_t hdr3 = (pl.type << 1) | pl.last;
   if (pl.type == 0) {
-    // stored: align, LEN, NLEN, raw bytes
-    uint64_t byte = (bit0 + 3 + 7) >> 3;  // relative to wbase
-    uint8_t* ob = reinterpret_cast<uint8_t*>(wbase);
-    uint32_t len = bi.stored_len;
-    uint32_t hdr4 = (len & 0xffff) | ((~len & 0xffff) << 16);
+    // stored: 3 header bits, pad to a byte, LEN, NLEN, raw bytes; bytes [B, E) relative to wbase
+    const uint64_t B = (bit0 + 3 + 7) >> 3;
+    const uint32_t len = bi.stored_len;
+    const uint32_t hdr4 = (len & 0xffff) | ((~len & 0xffff) << 16);
     const uint8_t* src = Ld.src + pl.byte_start;
-    // output byte range [byte, byte + 4 + len): word-granular writes
-    uint64_t b0 = byte, b1 = byte + 4 + len;
-    uint64_t w0 = b0 >> 2, w1 = (b1 + 3) >> 2;
+    const uint64_t E = B + 4 + len;
+    const uint64_t wl = (E - 1) >> 2;
+    const bool last_shared = (E & 3) != 0;
     const uintptr_t src_end = reinterpret_cast<uintptr_t>(src) + len;
-    for (uint64_t wi = w0 + threadIdx.x; wi < w1; wi += blockDim.x) {
-      // interior words: four input bytes from two aligned loads and a funnel shift
-      if (4 * wi >= b0 + 4 && 4 * wi + 4 <= b1) {
-        const uintptr_t ua = reinterpret_cast<uintptr_t>(src) + (4 * wi - b0 - 4);
+    for (uint64_t wi = wf + threadIdx.x; wi <= wl; wi += blockDim.x) {
+      uint32_t v = 0;
+      bool done = false;
+      if (4 * wi >= B + 4 && 4 * wi + 4 <= E) {  // interior: four input bytes, two aligned loads
+        const uintptr_t ua = reinterpret_cast<uintptr_t>(src) + (4 * wi - B - 4);
         const uintptr_t base = ua & ~uintptr_t(3);
         if (base + 8 <= src_end) {
           const uint32_t lo = __ldg(reinterpret_cast<const uint32_t*>(base));
           const uint32_t hi = __ldg(reinterpret_cast<const uint32_t*>(base) + 1);
-          reinterpret_cast<uint32_t*>(ob)[wi] = __funnelshift_r(lo, hi, 8 * (uint32_t)(ua & 3));
-          continue;
+          v = __funnelshift_r(lo, hi, 8 * (uint32_t)(ua & 3));
+          done = true;
         }
       }
-      uint32_t v = 0, mask = 0;
-      for (int k = 0; k < 4; k++) {
-        uint64_t ob_i = 4 * wi + k;
-        if (ob_i < b0 || ob_i >= b1) continue;
-        uint64_t r = ob_i - b0;
-        uint32_t byte_v = r < 4 ? (hdr4 >> (8 * r)) & 0xff : src[r - 4];
-        v |= byte_v << (8 * k);
-        mask |= 0xffu << (8 * k);
+      if (!done) {
+        for (int k = 0; k < 4; k++) {
+          const uint64_t ob = 4 * wi + k;
+          if (ob < B || ob >= E) continue;
+          const uint64_t r = ob - B;
+          const uint32_t byte_v = r < 4 ? (hdr4 >> (8 * r)) & 0xff : src[r - 4];
+          v |= byte_v << (8 * k);
+        }
       }
-      if (mask == 0xffffffffu) reinterpret_cast<uint32_t*>(ob)[wi] = v;
-      else atomicOr(&wbase[wi], v);
+      // the 3 header bits (then zero padding up to B); they straddle into word wf + 1 from bit 30 on
+      if (wi == wf) v |= hdr3 << (bit0 & 31);
+      if (wi == wf + 1 && (bit0 & 31) > 29) v |= hdr3 >> (32 - (bit0 & 31));
+      const bool is_lo = wi == wf && first_shared, is_hi = wi == wl && last_shared;
+      if (is_lo) edge[2 * slot] = make_uint2((uint32_t)wi, v);
+      else if (is_hi) edge[2 * slot + 1] = make_uint2((uint32_t)wi, v);
+      else wbase[wi] = v;
+    }
+    if (threadIdx.x == 0) {
+      if (!first_shared) edge[2 * slot] = make_uint2(EDGE_NONE, 0);
+      if (!last_shared || (wl == wf && first_shared)) edge[2 * slot + 1] = make_uint2(EDGE_NONE, 0);
     }
     return;
   }
@@ -1925,20 +1919,51 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const LaneDev* __restrict__
   const BlockCodes* bc = codes + slot;
   for (int i = threadIdx.x; i < (int)L_CODES; i += blockDim.x) s_l[i] = bc->l[i];
   for (int i = threadIdx.x; i < (int)D_CODES; i += blockDim.x) s_d[i] = bc->d[i];
-  uint64_t bit = bit0 + 3;
-  if (!stat) {
-    // dynamic tree description
+  if (threadIdx.x == 0) {
+    s_carry = 0;
+    s_lo = make_uint2(EDGE_NONE, 0);
+  }
+  // writes staged words [0, nwords) of a piece starting at absolute bit cbit (piece_bits long):
+  // complete words are stored (the shared first word becomes the lo contribution), a partial last
+  // word becomes the carry for the next piece
+  auto flush = [&](uint64_t cbit, uint32_t piece_bits) {
+    const uint32_t sh = (uint32_t)(cbit & 31);
+    const uint32_t nwords = (sh + piece_bits + 31) >> 5;
+    const bool partial_end = ((sh + piece_bits) & 31) != 0;
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
+      const uint64_t aw = (cbit >> 5) + i;
+      if (i == nwords - 1 && partial_end) s_carry = stage[i];
+      else if (aw == wf && first_shared) s_lo = make_uint2((uint32_t)aw, stage[i]);
+      else wbase[aw] = stage[i];
+    }
+  };
+  uint64_t bit = bit0;
+  __syncthreads();
+  {
+    // piece 0: the block header and (dynamic) the tree description, staged like a symbol chunk
+    const uint32_t hbits = stat ? 0u : bi.hdr_bits;
+    const uint32_t sh = (uint32_t)(bit & 31);
+    const uint32_t nwords = (sh + 3 + hbits + 31) >> 5;
+    for (uint32_t i = threadIdx.x; i < nwords + 1; i += blockDim.x) stage[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicOr(&stage[0], hdr3 << sh);
+      if (sh > 29) atomicOr(&stage[1], hdr3 >> (32 - sh));  // the header straddles a word
+    }
     const uint32_t* hb = hdr + (uint64_t)slot * (HDR_BYTES / 4);
-    uint32_t hbits = bi.hdr_bits;
     for (uint32_t i = threadIdx.x; i * 32 < hbits; i += blockDim.x) {
-      uint32_t l = min(32u, hbits - i * 32);
+      const uint32_t l = min(32u, hbits - i * 32);
       uint64_t v = hb[i];
       if (l < 32) v &= (1ull << l) - 1;
-      or_bits_global(wbase, bit + 32ull * i, v, l);
+      const uint32_t o = sh + 3 + 32 * i, wi = o >> 5, ob = o & 31;
+      atomicOr(&stage[wi], (uint32_t)(v << ob));
+      if (ob + l > 32) atomicOr(&stage[wi + 1], (uint32_t)(v >> (32 - ob)));
     }
-    bit += hbits;
+    __syncthreads();
+    flush(bit, 3 + hbits);
+    bit += 3 + hbits;
+    __syncthreads();
   }
-  __syncthreads();
   const uint32_t* sy = syms + Ld.sym_base + bi.sym0;
   const uint32_t total = bi.nsym + 1;  // + END_BLOCK
   const uint32_t eob_code = stat ? c_z.sl_code[256] : (s_l[256] & 0xffff);
@@ -1965,7 +1990,7 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const LaneDev* __restrict__
     const uint64_t cbit = bit;  // chunk start (absolute, rel. wbase)
     const uint32_t sh = (uint32_t)(cbit & 31);
     const uint32_t nwords = (sh + chunk_bits + 31) >> 5;
-    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) stage[i] = 0;
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) stage[i] = (i == 0 && sh) ? s_carry : 0u;
     __syncthreads();
     uint32_t o = sh + toff;
 #pragma unroll
@@ -1979,15 +2004,57 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const LaneDev* __restrict__
       }
     }
     __syncthreads();
-    uint32_t* gw = wbase + (cbit >> 5);
-    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
-      bool edge = (i == 0 && sh != 0) || (i == nwords - 1 && ((sh + chunk_bits) & 31) != 0);
-      if (edge) atomicOr(&gw[i], stage[i]);
-      else gw[i] = stage[i];
-    }
+    flush(cbit, chunk_bits);
     bit += chunk_bits;
     __syncthreads();
   }
+  if (threadIdx.x == 0) {
+    // the block's last word: partial iff the block ends mid-word (then it is the carry)
+    uint2 hi = make_uint2(EDGE_NONE, 0);
+    uint2 lo = s_lo;
+    if (bit & 31) {
+      const uint64_t wl = (bit - 1) >> 5;
+      if (wl == wf && first_shared) lo = make_uint2((uint32_t)wl, s_carry);
+      else hi = make_uint2((uint32_t)wl, s_carry);
+    }
+    edge[2 * slot] = lo;
+    edge[2 * slot + 1] = hi;
+  }
+}
+
+// one thread per edge contribution; the first contribution of each word ORs the run of
+// contributions to that word (blocks are contiguous, so they are adjacent in slot order) and
+// stores it
+__global__ void k_edges(const LaneDev* __restrict__ lanes, const uint32_t* __restrict__ blk_lane,
+                        uint32_t nblk_slots, const LaneSyms* __restrict__ ls, uint8_t* const* __restrict__ lane_out,
+                        const uint2* __restrict__ edge) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t slot = t >> 1;
+  if (slot >= nblk_slots) return;
+  const uint32_t li = blk_lane[slot];
+  const LaneDev Ld = lanes[li];
+  const uint32_t nb = ls[li].nblk;
+  if (slot - Ld.blk0 >= nb) return;
+  uint8_t* out = lane_out[li];
+  if (!out) return;
+  const uint2 me = edge[t];
+  if (me.x == EDGE_NONE) return;
+  const uint32_t t0 = 2 * Ld.blk0, t1 = 2 * (Ld.blk0 + nb);  // this lane's contributions
+  for (uint32_t u = t; u-- > t0;) {  // an earlier contribution to the same word owns it
+    const uint32_t x = edge[u].x;
+    if (x == EDGE_NONE) continue;
+    if (x == me.x) return;
+    break;
+  }
+  uint32_t v = me.y;
+  for (uint32_t u = t + 1; u < t1; u++) {
+    const uint2 c = edge[u];
+    if (c.x == EDGE_NONE) continue;
+    if (c.x != me.x) break;
+    v |= c.y;
+  }
+  uint32_t* wbase = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(out) & ~uintptr_t(3));
+  wbase[me.x] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -2090,13 +2157,15 @@ __global__ void k_adler_final(const LaneDev* __restrict__ lanes, int nlanes, con
   uint32_t a = (1 + acc.A) % MOD;
   uint32_t b = (uint32_t)((Ld.n % MOD + acc.B) % MOD);
   uint32_t ad = (b << 16) | a;
-  uintptr_t addr = reinterpret_cast<uintptr_t>(out);
-  uint32_t* wbase = reinterpret_cast<uint32_t*>(addr & ~uintptr_t(3));
-  uint64_t bit = 8ull * (addr & 3);
-  or_bits_global(wbase, bit, 0x9c78u, 16);  // 78 9C, LSB first
-  uint64_t tail = bit + 8ull * (blob_len[li] - 4);
-  uint32_t be = ((ad >> 24) & 0xff) | (((ad >> 16) & 0xff) << 8) | (((ad >> 8) & 0xff) << 16) | ((ad & 0xff) << 24);
-  or_bits_global(wbase, tail, be, 32);
+  // zlib header 78 9C and the big-endian Adler-32 trailer, as byte stores (they share words with the
+  // blocks' edge words and the container header, all written by earlier kernels)
+  out[0] = 0x78;
+  out[1] = 0x9c;
+  uint8_t* tail = out + blob_len[li] - 4;
+  tail[0] = (uint8_t)(ad >> 24);
+  tail[1] = (uint8_t)(ad >> 16);
+  tail[2] = (uint8_t)(ad >> 8);
+  tail[3] = (uint8_t)ad;
 }
 
 __global__ void k_container_header(const ContainerDev* __restrict__ cons, int ncons,
@@ -2114,10 +2183,7 @@ __global__ void k_container_header(const ContainerDev* __restrict__ cons, int nc
     h[15 + i] = (uint8_t)(hl >> (8 * i));
     h[23 + i] = (uint8_t)(ll >> (8 * i));
   }
-  uintptr_t addr = reinterpret_cast<uintptr_t>(C.dst);
-  uint32_t* wbase = reinterpret_cast<uint32_t*>(addr & ~uintptr_t(3));
-  uint64_t bit = 8ull * (addr & 3);
-  for (int i = 0; i < BB_CONTAINER_HEADER; i++) or_bits_global(wbase, bit + 8ull * i, h[i], 8);
+  for (int i = 0; i < BB_CONTAINER_HEADER; i++) C.dst[i] = h[i];
 }
 
 }  // namespace
@@ -2236,7 +2302,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   need += 5 * al(sizeof(SegExit) * seg_total) + 6 * al(4ull * seg_total) + al(8ull * seg_total);
   need += al(4 * sym_total);
   need += al(sizeof(LaneSyms) * nl) + al(sizeof(BlockInfo) * blk_total) + al(sizeof(BlockCodes) * blk_total);
-  need += al(HDR_BYTES * (size_t)blk_total) + al(sizeof(BlockPlan) * blk_total);
+  need += al(HDR_BYTES * (size_t)blk_total) + al(sizeof(BlockPlan) * blk_total) + al(16ull * blk_total);
   need += al(8 * nl) + al(sizeof(uint8_t*) * nl) + al(8 * nc) + al(4 * nc) + al(sizeof(Adl) * ad_work.size() + 16);
   need += 64 * 256 + 2 * al(8 * (nl + 1)) + al(4 * nl) + al(sizeof(WorkItem) * (pos_total / HP4_SEG + nl + 1));
   int rc = e->ws.reserve(need);
@@ -2272,6 +2338,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BlockCodes* d_codes = W.take<BlockCodes>(blk_total);
   uint32_t* d_hdr = W.take<uint32_t>((size_t)blk_total * (HDR_BYTES / 4));
   BlockPlan* d_plan = W.take<BlockPlan>(blk_total);
+  uint2* d_edge = W.take<uint2>(2ull * blk_total);
   uint64_t* d_blob_len = W.take<uint64_t>(nl);
   uint8_t** d_lane_out = W.take<uint8_t*>(nl);
   uint64_t* d_con_len = W.take<uint64_t>(nc);
@@ -2368,21 +2435,16 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     k_blocks<BK_THREADS><<<blk_total, BK_THREADS, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_syms, d_info,
                                                            d_codes, d_hdr);
   BB_LAUNCH_CHECK();
-  T.mark("deflate.layout_zero");
+  T.mark("deflate.layout");
   k_layout<<<(nl + 3) / 4, 128, 0, st>>>(d_lanes, nl, d_ls, d_info, d_plan, d_blob_len);
   BB_LAUNCH_CHECK();
   k_place<<<(nc + 127) / 128, 128, 0, st>>>(d_cons, nc, d_blob_len, d_lane_out, d_con_len, d_con_status);
   BB_LAUNCH_CHECK();
-  uint64_t max_bound = 0;
-  for (int c = 0; c < nc; c++) max_bound = std::max<uint64_t>(max_bound, containers[c].cap);
-  {
-    dim3 g((unsigned)std::min<uint64_t>(std::max<uint64_t>(1, max_bound / (16 * 256) + 1), 1184), nc);
-    k_zero<<<g, 256, 0, st>>>(d_cons, d_con_len, d_con_status);
-    BB_LAUNCH_CHECK();
-  }
   T.mark("deflate.emit");
   k_emit<<<blk_total, EM_THREADS, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_info, d_plan, d_codes, d_hdr,
-                                           d_syms, d_lane_out);
+                                           d_syms, d_lane_out, d_edge);
+  BB_LAUNCH_CHECK();
+  k_edges<<<(2 * blk_total + 255) / 256, 256, 0, st>>>(d_lanes, d_blk_lane, blk_total, d_ls, d_lane_out, d_edge);
   BB_LAUNCH_CHECK();
   T.mark("deflate.adler_finalize");
   if (!ad_work.empty()) {
