@@ -315,3 +315,34 @@ def test_parallel_inflate_long_copy_chains(codec):
         bad[len(bad) // 2] ^= 0x10
         with pytest.raises(codec.CorruptContainer):
             dec(bytes(bad), n)
+
+
+def test_parallel_inflate_checks_the_zlib_header(codec, oracle):
+    """lanes of >= 64 KiB take the parallel inflate, which starts decoding at bit 16; a bad
+    CMF / FLG (FCHECK, CM != 8, CINFO > 7, FDICT set with a valid FCHECK) must still be rejected, as
+    zlib's uncompress does (inflate.c HEAD state; reference codec.cpp:27-38)."""
+    from oracle.oracle import OracleError
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    data = oracle.synth_bf16(300000, 12)
+    base = bytearray(zlib.compress(data, 6))
+    assert len(base) >= 1 << 16 and bytes(base[:2]) == b"\x78\x9c"
+
+    def fcheck(cmf, flg_hi):  # FLG with FCHECK making (CMF * 256 + FLG) % 31 == 0
+        flg = flg_hi & 0xe0
+        return flg | (31 - ((cmf << 8) | flg) % 31) % 31
+
+    cases = {
+        "fcheck": (0x78, 0x9d),
+        "cm": (0x77, fcheck(0x77, 0x80)),
+        "cinfo": (0x88, fcheck(0x88, 0x80)),
+        "fdict": (0x78, fcheck(0x78, 0xa0)),
+    }
+    for name, (cmf, flg) in cases.items():
+        blob = bytes([cmf, flg]) + bytes(base[2:])
+        with pytest.raises(OracleError):
+            oracle.zlib_uncompress(blob, len(data))
+        with pytest.raises(zlib.error):  # the pinned system zlib agrees
+            zlib.decompress(blob)
+        with pytest.raises(codec.CorruptContainer):
+            dec(blob, len(data))
+    assert dec(bytes(base), len(data)) == data
