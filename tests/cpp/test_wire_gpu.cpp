@@ -167,3 +167,28 @@ TEST_CASE("TCP roles: source -> stage -> sink over loopback sockets, codec on th
   ::close(stage_fd);
   ::close(sink_fd);
 }
+
+TEST_CASE("GPU runner: identity backend, empty micro-batches and zero steps") {
+  WireLocalConfig cfg = relay(1, 4, 4, true);  // 2 elements over 4 micro-batches: two empty spans
+  cfg.backend = kBackendIdentity;
+  WireLocalResult r = run_wire_local(cfg);
+  CHECK(r.sink.payload_ok);
+  CHECK(r.sink.frames_seen == 8);
+  WireLocalConfig none = relay(2, 2, 1 << 16, true);
+  none.steps = 0;
+  WireLocalResult z = run_wire_local(none);
+  CHECK(z.sink.payload_ok);
+  CHECK(z.sink.frames_seen == 0);
+  CHECK(z.end_to_end_ms == 0.0);
+}
+
+TEST_CASE("GPU runner: queue_slots = 1 and a long relay keep every frame in order") {
+  b200::WireLocalOptions opt;
+  opt.queue_slots = 1;
+  WireLocalConfig cfg = relay(5, 6, 3 << 20, true);
+  cfg.steps = 3;
+  WireLocalResult r = b200::run_wire_local(cfg, opt);
+  CHECK(r.sink.payload_ok);
+  CHECK(r.sink.frames_seen == 18);
+  for (const HopMetrics& h : r.hops) CHECK(h.frames == 18);
+}
