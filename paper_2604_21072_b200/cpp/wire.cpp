@@ -534,8 +534,13 @@ class RoleDevice {
 // and releases a slot once the frame's bytes are no longer needed.
 class Inbox {
  public:
-  Inbox(int dev, int slots) : dev_(dev), bufs_(static_cast<std::size_t>(slots)) {
-    for (int i = 0; i < slots; ++i) free_.push_back(i);
+  // every slot is allocated up front at the run's largest frame: no cudaMalloc / cudaFree (which
+  // synchronizes the whole device) happens once frames flow
+  Inbox(int dev, int slots, std::size_t slot_bytes) : dev_(dev), bufs_(static_cast<std::size_t>(slots)) {
+    for (int i = 0; i < slots; ++i) {
+      bufs_[static_cast<std::size_t>(i)].ensure(dev, slot_bytes);
+      free_.push_back(i);
+    }
   }
   int dev() const { return dev_; }
   int acquire(std::size_t bytes) {
@@ -592,8 +597,11 @@ class Inbox {
 // pool of reusable device buffers of one role (decoded payloads, outbound frames)
 class BufPool {
  public:
-  BufPool(int dev, int n) : dev_(dev), bufs_(static_cast<std::size_t>(n)) {
-    for (int i = 0; i < n; ++i) free_.push_back(i);
+  BufPool(int dev, int n, std::size_t bytes) : dev_(dev), bufs_(static_cast<std::size_t>(n)) {
+    for (int i = 0; i < n; ++i) {
+      bufs_[static_cast<std::size_t>(i)].ensure(dev, bytes);
+      free_.push_back(i);
+    }
   }
   int take(std::size_t bytes) {
     std::unique_lock<std::mutex> lk(mu_);
@@ -696,7 +704,7 @@ class HopSender {
   void warm(RoleDevice& rd) {
     DevBuf scratch;
     scratch.ensure(rd.dev(), 256);
-    const int s = to_.acquire(256);
+    const int s = to_.acquire(256);  // slots are pre-sized: no reallocation
     cudaError_t e = to_.dev() == rd.dev()
                         ? cudaMemcpyAsync(to_.slot(s), scratch.get(), 256, cudaMemcpyDeviceToDevice, rd.stream())
                         : cudaMemcpyPeerAsync(to_.slot(s), to_.dev(), scratch.get(), rd.dev(), 256, rd.stream());
@@ -1047,11 +1055,18 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
   }
   host_streams.clear();
 
+  const std::size_t frame_cap = [&] {
+    std::size_t mx = 0;
+    for (const auto& sp : spans) mx = std::max(mx, sp.second);
+    return std::max(mx, static_cast<std::size_t>(bb_compress_bound(mx, cfg.backend, 1)));
+  }();
   const int slots = std::max(1, opt.queue_slots);
   // inbox[i] receives hop i (i = 0: source -> first receiver); its slots cover what the receiver
   // may hold at once: its queues, the frame in compute and the frame on the outbound link
   std::vector<std::unique_ptr<Inbox>> inbox;
-  for (int r = 1; r < roles; ++r) inbox.push_back(std::make_unique<Inbox>(role_dev[static_cast<std::size_t>(r)], 2 * slots + 3));
+  for (int r = 1; r < roles; ++r)
+    inbox.push_back(std::make_unique<Inbox>(role_dev[static_cast<std::size_t>(r)], 2 * slots + 3,
+                                            kFrameHeaderSize + frame_cap + 16));
   const WireFault* fault = opt.fault.kind == WireFault::Kind::None ? nullptr : &opt.fault;
   auto fault_for = [&](int hop) { return fault && fault->hop == hop ? fault : nullptr; };
   std::vector<std::unique_ptr<HopSender>> hop;
@@ -1062,7 +1077,8 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
   result.stages.resize(static_cast<std::size_t>(cfg.stage_count));
   FirstFailure failure;
   std::vector<std::unique_ptr<BufPool>> pools;
-  for (int i = 0; i < cfg.stage_count; ++i) pools.push_back(std::make_unique<BufPool>(role_dev[static_cast<std::size_t>(i) + 1], slots + 4));
+  for (int i = 0; i < cfg.stage_count; ++i)
+    pools.push_back(std::make_unique<BufPool>(role_dev[static_cast<std::size_t>(i) + 1], slots + 4, frame_cap + 16));
   // a failing role unblocks both neighbours: its inbox (upstream sender) and its outbound hop
   auto close_role = [&](int r) {
     if (r >= 1) inbox[static_cast<std::size_t>(r) - 1]->close();
@@ -1077,12 +1093,6 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
   Latch ready(2 + 2 * cfg.stage_count);
   std::size_t warm_bytes = 0;
   for (const auto& sp : spans) warm_bytes = std::max(warm_bytes, sp.second);
-  const std::uint8_t backend = cfg.backend;
-  const std::size_t frame_cap = [&] {
-    std::size_t mx = 0;
-    for (const auto& sp : spans) mx = std::max(mx, sp.second);
-    return std::max(mx, static_cast<std::size_t>(bb_compress_bound(mx, backend, 1)));
-  }();
 
   std::vector<std::thread> threads;
   // sink (wire.cpp:543-602): reassemble every step in HBM and compare with the expected stream

@@ -1195,6 +1195,16 @@ __global__ void k_parse_fixup(const LaneDev* __restrict__ lanes, const uint32_t*
   if (old.p != ex.p || old.state != ex.state) atomicAdd(changed, 1u);
 }
 
+// the fresh state each speculative parse assumed: segment k of a lane starts at k * G with
+// prev_length = MIN_MATCH - 1, no pending literal (written on the device: no host round trip)
+__global__ void k_fresh_entries(const LaneDev* __restrict__ lanes, const uint32_t* __restrict__ seg_lane,
+                                uint32_t nseg_total, SegExit* __restrict__ entry_used) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nseg_total) return;
+  const LaneDev Ld = lanes[seg_lane[g]];
+  entry_used[g] = SegExit{(g - Ld.seg0) * Ld.G, 0x80000000u | (MIN_MATCH - 1)};
+}
+
 // ---------------------------------------------------------------------------
 // K6a: per-lane symbol offsets of every segment (one CTA per lane)
 struct LaneSyms {
@@ -2389,14 +2399,8 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
                                   d_spec_exit, d_spec_cnt, d_spec_post, sym_stride);
   BB_LAUNCH_CHECK();
   // entry_used = the fresh state each speculative parse assumed
-  {
-    std::vector<SegExit> fresh(seg_total);
-    for (int i = 0; i < nl; i++)
-      for (uint32_t k = 0; k < L[i].nseg; k++)
-        fresh[L[i].seg0 + k] = SegExit{(uint32_t)((uint64_t)k * L[i].G), 0x80000000u | (MIN_MATCH - 1)};
-    BB_CUDA_TRY(cudaMemcpyAsync(d_entry_used, fresh.data(), sizeof(SegExit) * seg_total, cudaMemcpyHostToDevice, st));
-    BB_CUDA_TRY(cudaStreamSynchronize(st));  // `fresh` is pageable
-  }
+  k_fresh_entries<<<(seg_total + 255) / 256, 256, 0, st>>>(d_lanes, d_seg_lane, seg_total, d_entry_used);
+  BB_LAUNCH_CHECK();
   BB_CUDA_TRY(cudaMemcpyAsync(d_exit_a, d_spec_exit, sizeof(SegExit) * seg_total, cudaMemcpyDeviceToDevice, st));
   BB_CUDA_TRY(cudaMemsetAsync(d_fix_cnt, 0, 4ull * seg_total, st));
   BB_CUDA_TRY(cudaMemsetAsync(d_conv_idx, 0, 4ull * seg_total, st));
@@ -2404,14 +2408,17 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   if ((rc = pinned(e, 64 + 16ull * nc))) return rc;
   T.mark("deflate.parse_fixup");
   SegExit *cur = d_exit_a, *nxt = d_exit_b;
-  for (int round = 0;; round++) {
-    BB_CUDA_TRY(cudaMemsetAsync(d_changed, 0, 4, st));
-    k_parse_fixup<<<pg, pt, 0, st>>>(d_lanes, d_seg_lane, seg_total, d_prof, d_state_map, d_spec_exit,
-                                     d_spec_cnt, d_spec_post, cur, nxt, d_entry_used, d_fix_syms, d_fix_cnt,
-                                     d_conv_idx, d_post_flag, d_changed, sym_stride);
-    BB_LAUNCH_CHECK();
-    std::swap(cur, nxt);
-    BB_CUDA_TRY(cudaMemcpyAsync(e->h_pinned, d_changed, 4, cudaMemcpyDeviceToHost, st));
+  // two rounds per host check (a round after convergence only copies the exits): half the syncs
+  for (int round = 0;; round += 2) {
+    BB_CUDA_TRY(cudaMemsetAsync(d_changed, 0, 8, st));
+    for (int r = 0; r < 2; r++) {
+      k_parse_fixup<<<pg, pt, 0, st>>>(d_lanes, d_seg_lane, seg_total, d_prof, d_state_map, d_spec_exit,
+                                       d_spec_cnt, d_spec_post, cur, nxt, d_entry_used, d_fix_syms, d_fix_cnt,
+                                       d_conv_idx, d_post_flag, d_changed + r, sym_stride);
+      BB_LAUNCH_CHECK();
+      std::swap(cur, nxt);
+    }
+    BB_CUDA_TRY(cudaMemcpyAsync(e->h_pinned, d_changed + 1, 4, cudaMemcpyDeviceToHost, st));
     BB_CUDA_TRY(cudaStreamSynchronize(st));
     uint32_t changed = *reinterpret_cast<uint32_t*>(e->h_pinned);
     if (changed == 0) break;
