@@ -753,17 +753,18 @@ std::size_t container_decoded_size(RoleDevice& rd, const std::uint8_t* c, std::s
   return need;
 }
 
-// one compress + decompress of a buffer of `bytes` on the role's context: loads the codec's kernels
-// on this device and grows the context's workspaces to the run's frame size
-void warm_codec(RoleDevice& rd, std::size_t bytes, std::uint8_t backend) {
+// one compress + decompress of a micro-batch of the run's own data on the role's context: loads the
+// codec's kernels on this device and grows the context's workspaces to what the run's frames need
+// (a workspace that grows while frames flow costs a device-synchronising cudaFree)
+void warm_codec(RoleDevice& rd, const Bytes& sample, std::uint8_t backend) {
+  std::size_t bytes = sample.size() & ~std::size_t(1);
   if (bytes < 2) return;
-  bytes &= ~std::size_t(1);
   DevBuf in, out, back;
   const std::size_t cap = bb_compress_bound(bytes, backend, 1);
   in.ensure(rd.dev(), bytes);
   out.ensure(rd.dev(), cap);
   back.ensure(rd.dev(), bytes);
-  WIRE_CUDA(cudaMemsetAsync(in.get(), 0x3c, bytes, rd.stream()));
+  WIRE_CUDA(cudaMemcpyAsync(in.get(), sample.data(), bytes, cudaMemcpyHostToDevice, rd.stream()));
   std::size_t len = 0, got = 0;
   codec_ok(bb_compress(rd.ctx(), in.get(), bytes, backend, 1, out.get(), cap, &len, rd.stream()));
   codec_ok(bb_decompress(rd.ctx(), out.get(), len, back.get(), bytes, &got, rd.stream()));
@@ -1053,6 +1054,15 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     WIRE_CUDA(cudaMemcpy(src_streams[static_cast<std::size_t>(s)].get(), h.data(), h.size(), cudaMemcpyHostToDevice));
     WIRE_CUDA(cudaMemcpy(want_streams[static_cast<std::size_t>(s)].get(), h.data(), h.size(), cudaMemcpyHostToDevice));
   }
+  // the warm-up sample: the largest micro-batch of the first step
+  Bytes warm_sample;
+  if (steps > 0) {
+    std::size_t off = 0, len = 0;
+    for (const auto& sp : spans)
+      if (sp.second > len) off = sp.first, len = sp.second;
+    warm_sample.assign(host_streams[0].begin() + static_cast<std::ptrdiff_t>(off),
+                       host_streams[0].begin() + static_cast<std::ptrdiff_t>(off + len));
+  }
   host_streams.clear();
 
   const std::size_t frame_cap = [&] {
@@ -1091,8 +1101,6 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
   };
   // source, sink, and per stage its compute and send workers warm up (codec, first peer copy)
   Latch ready(2 + 2 * cfg.stage_count);
-  std::size_t warm_bytes = 0;
-  for (const auto& sp : spans) warm_bytes = std::max(warm_bytes, sp.second);
 
   std::vector<std::thread> threads;
   // sink (wire.cpp:543-602): reassemble every step in HBM and compare with the expected stream
@@ -1101,7 +1109,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     try {
       Arrival arrival(ready);
       RoleDevice rd(sink_dev);
-      if (cfg.compress) warm_codec(rd, warm_bytes, cfg.backend);
+      if (cfg.compress) warm_codec(rd, warm_sample, cfg.backend);
       arrival.now();
       Inbox& in = *inbox.back();
       WireRoleReport& rep = result.sink;
@@ -1225,7 +1233,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
         try {
           Arrival arrival(ready);
           RoleDevice rd(dev);
-          if (cfg.compress) warm_codec(rd, warm_bytes, cfg.backend);
+          if (cfg.compress) warm_codec(rd, warm_sample, cfg.backend);
           arrival.now();
           for (;;) {
             DevFrame f = inbound.pop().value_or(shutdown());
@@ -1327,7 +1335,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     const int r = 0;
     try {
       RoleDevice rd(src_dev);
-      if (cfg.compress) warm_codec(rd, warm_bytes, cfg.backend);
+      if (cfg.compress) warm_codec(rd, warm_sample, cfg.backend);
       hop.front()->warm(rd);
       ready.arrive();
       ready.wait();  // every role is up (or failed): the first offer starts end_to_end_ms

@@ -132,6 +132,12 @@ bool try_register(const void* p, size_t n) {
   return true;
 }
 
+// BB_HOSTIO_DIRECT=1: plain cudaMemcpyAsync from / to pageable memory (the driver's own staging)
+bool direct_only() {
+  static const bool d = getenv("BB_HOSTIO_DIRECT") != nullptr;
+  return d;
+}
+
 bool page_locked(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -161,7 +167,7 @@ int HostStager::ready() {
 
 int HostStager::h2d(uint8_t* d_dst, const uint8_t* h_src, size_t n, cudaStream_t st) {
   if (!n) return BB_OK;
-  if (n < SMALL || page_locked(h_src)) {
+  if (n < SMALL || direct_only() || page_locked(h_src)) {
     BB_CUDA_TRY(cudaMemcpyAsync(d_dst, h_src, n, cudaMemcpyHostToDevice, st));
     return BB_OK;
   }
@@ -187,7 +193,7 @@ int HostStager::h2d(uint8_t* d_dst, const uint8_t* h_src, size_t n, cudaStream_t
 
 int HostStager::d2h(uint8_t* h_dst, const uint8_t* d_src, size_t n, cudaStream_t st) {
   if (!n) return BB_OK;
-  if (n < SMALL || page_locked(h_dst)) {
+  if (n < SMALL || direct_only() || page_locked(h_dst)) {
     BB_CUDA_TRY(cudaMemcpyAsync(h_dst, d_src, n, cudaMemcpyDeviceToHost, st));
     return BB_OK;
   }
