@@ -551,6 +551,9 @@ __device__ __forceinline__ uint32_t pf_pick(const uint32_t (&c)[B], int t) {
 }
 
 constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;
+#ifdef PF_STATS
+__device__ unsigned long long g_pf_stats[4];  // flushes, recorded candidates, warp flush iterations, batches
+#endif
 #ifndef PF_B1
 #define PF_B1 8  // chain steps per batch within the first 32 (budget-32 snapshot)
 #endif
@@ -659,6 +662,39 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     // a head exactly at MAX_DIST is still compared, and every later candidate is below it
     const uint32_t lim4 = 4 * lim1 - (live && c0 == lim1 ? 4u : 0u);
     const uint32_t qw2 = p < e ? w32[ip1 + 2] : 0u;  // bytes p + 2, p + 3 (wlen covers e + 274)
+#ifndef PF_NO_HEAD_SEED
+    // The head candidate (chain step 1) is extended exactly before the walk, so best starts at its
+    // length: the batches' quick test then records only candidates that can beat it (with best = 2,
+    // every same-3-gram candidate of the first batch was recorded and extended in the flush).  The
+    // head is first in chain order, so seeding best with it leaves the first maximum unchanged; its
+    // own step in the first batch fails the quick test (its byte `best` mismatches) or re-tests to no
+    // change.
+    if (live && ((w32[c0] ^ wp) & 0xffff0000u) == 0) {
+      uint32_t len = 2;
+      const uint32_t x2 = (w32[c0 + 2] ^ qw2) >> 16;
+      if (x2) {
+        len += (x2 & 0xff) == 0;
+      } else {
+        len = 4;
+        while (len < maxl) {
+          const uint32_t x = (w32[c0 + len] ^ w32[ip1 + len]) >> 16;
+          if (x) {
+            len += (x & 0xff) == 0;
+            break;
+          }
+          len += 2;
+        }
+      }
+      len = min(len, maxl);
+      if (len > best) {
+        best = len;
+        bestd = d0;
+        offb = sw + 4 * (best - 1) + 2;
+        key = (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u);
+        if (len >= nice) ic4 = 0;  // zlib stops at nice_match: the lane walks the dead sentinel
+      }
+    }
+#endif
     // one batch of B chain steps, then the recorded candidates in chain order
     auto batch = [&](auto bsize) {
       constexpr int B = decltype(bsize)::value;
@@ -686,6 +722,17 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
         ic4 = (wc << 2) & 0x3fffc;
       }
       if (__any_sync(0xffffffffu, mask != 0)) {
+#ifdef PF_STATS
+        {
+          const uint32_t rec = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mask));
+          const uint32_t mx = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(mask));
+          if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&g_pf_stats[0], 1ull);                      // flushes
+            atomicAdd(&g_pf_stats[1], (unsigned long long)rec);   // recorded candidates
+            atomicAdd(&g_pf_stats[2], (unsigned long long)mx);    // warp iterations (max popc)
+          }
+        }
+#endif
         bool improved = false;
         while (mask) {
           const int t = __ffs(mask) - 1;
@@ -729,11 +776,17 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     };
     for (int cnt = 0; cnt < 32; cnt += PF_B1) {
       if (!__any_sync(0xffffffffu, ic4 > lim4)) break;
+#ifdef PF_STATS
+      if ((threadIdx.x & 31) == 0) atomicAdd(&g_pf_stats[3], 1ull);
+#endif
       batch(std::integral_constant<int, PF_B1>());
     }
     const uint32_t r32 = prof_pack(best, bestd);  // budget 32 (prev_length >= good_length)
     for (int cnt = 32; cnt < (int)MAX_CHAIN; cnt += PF_B2) {
       if (!__any_sync(0xffffffffu, ic4 > lim4)) break;
+#ifdef PF_STATS
+      if ((threadIdx.x & 31) == 0) atomicAdd(&g_pf_stats[3], 1ull);
+#endif
       batch(std::integral_constant<int, PF_B2>());
     }
     if (p < e) {
@@ -2476,6 +2529,16 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
 }
 
 }  // namespace bb
+
+#ifdef PF_STATS
+extern "C" BB_API void bb_debug_pf_stats(unsigned long long* out4, int reset) {
+  cudaMemcpyFromSymbol(out4, bb::g_pf_stats, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(bb::g_pf_stats, z, sizeof z);
+  }
+}
+#endif
 
 // Test hook: K3S + K4S alone on one lane (profiles without the parse's byte), for the
 // comparison with the oracle's orc_match_profile.
