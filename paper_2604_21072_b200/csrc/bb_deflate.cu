@@ -2327,7 +2327,10 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
 #ifndef K5_G_BIG
 #define K5_G_BIG 4096
 #endif
-    d.G = j.n <= (1u << 20) ? 256 : j.n <= (4u << 20) ? 1024 : K5_G_BIG;  // small lanes: more, shorter parse segments
+#ifndef K5_G_SMALL
+#define K5_G_SMALL 128  // config1: parse 0.192 -> 0.116 ms (64: 0.092 ms but more fix-up, 2.431 vs 2.376 ms per round trip)
+#endif
+    d.G = j.n <= (1u << 20) ? K5_G_SMALL : j.n <= (4u << 20) ? 1024 : K5_G_BIG;  // small lanes: more, shorter parse segments
     d.seg0 = seg_total;
     d.nseg = (uint32_t)std::max<uint64_t>(1, (j.n + d.G - 1) / d.G);
     d.blk0 = blk_total;
