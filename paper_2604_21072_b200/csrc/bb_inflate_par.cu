@@ -902,10 +902,17 @@ struct WarpSm {
   uint16_t rnm[32][REC];   // matches before record j
 };
 
+// Two register budgets: MINB 5 (127 registers, no spills) has the shortest latency per block
+// (config1's few blocks: 0.39 vs 0.48 ms with the other); MINB 16 (64 registers, small spills)
+// has 3x the resident warps and the best throughput over many blocks (config2: 3.53 vs 3.82 ms).
 #ifndef DS_MINB
 #define DS_MINB 5
 #endif
-__global__ void __launch_bounds__(32 * WD_WARPS, DS_MINB) k_dyn_scan(const PJob* __restrict__ jobs,
+#ifndef DS_MINB_WIDE
+#define DS_MINB_WIDE 16
+#endif
+template <int MINB>
+__global__ void __launch_bounds__(32 * WD_WARPS, MINB) k_dyn_scan(const PJob* __restrict__ jobs,
                                                            const uint32_t* __restrict__ node_job,
                                                            const uint32_t* __restrict__ dyn_nodes, uint32_t ndyn_total,
                                                            Node* __restrict__ nodes, Tables* __restrict__ tabs,
@@ -1997,7 +2004,9 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
       BB_CUDA_TRY(cudaFuncSetAttribute(k_decode_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nd_smem));
       BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_local, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_SMEM));
       BB_CUDA_TRY(cudaFuncSetAttribute(k_resolve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, RS_SMEM));
-      BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan<DS_MINB_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(WarpSm) * WD_WARPS)));
+      BB_CUDA_TRY(cudaFuncSetAttribute(k_dyn_scan<DS_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(WarpSm) * WD_WARPS)));
       attr_done[dev] = true;
     }
@@ -2200,7 +2209,12 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
                                                                                       d_nodes);
   BB_LAUNCH_CHECK();
   if (ndyn_total) {
-    k_dyn_scan<<<(ndyn_total + WD_WARPS - 1) / WD_WARPS, 32 * WD_WARPS, sizeof(WarpSm) * WD_WARPS, st>>>(
+    const unsigned ds_grid = (ndyn_total + WD_WARPS - 1) / WD_WARPS;
+    if (ndyn_total >= 4u * kNumSMs * WD_WARPS)
+      k_dyn_scan<DS_MINB_WIDE><<<ds_grid, 32 * WD_WARPS, sizeof(WarpSm) * WD_WARPS, st>>>(
+        d_jobs, d_node_job, d_dyn_nodes, ndyn_total, d_nodes, d_dtabs, d_plans, d_extra);
+    else
+      k_dyn_scan<DS_MINB><<<ds_grid, 32 * WD_WARPS, sizeof(WarpSm) * WD_WARPS, st>>>(
         d_jobs, d_node_job, d_dyn_nodes, ndyn_total, d_nodes, d_dtabs, d_plans, d_extra);
     BB_LAUNCH_CHECK();
   }
