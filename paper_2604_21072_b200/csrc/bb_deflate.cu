@@ -29,6 +29,7 @@
 //   K7 k_emit         parallel bit packing of every block into the container
 //      k_adler*       Adler-32 (chunk sums + ordered combine), zlib header/trailer,
 //      k_finalize     BBC1 header
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
@@ -42,6 +43,7 @@
 #include "bb_kernels.h"
 
 namespace bb {
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -1181,17 +1183,19 @@ __global__ void k_parse_spec(const LaneDev* __restrict__ lanes, int nlanes,
 
 // One Jacobi round: every segment re-derives its result from its predecessor's
 // current exit state.  A segment whose entry is unchanged is skipped.
-__global__ void k_parse_fixup(const LaneDev* __restrict__ lanes, const uint32_t* __restrict__ seg_lane,
-                              uint32_t nseg_total, const uint2* __restrict__ prof,
-                              const uint2* __restrict__ state_map, const SegExit* __restrict__ spec_exit,
-                              const uint32_t* __restrict__ spec_cnt, const uint32_t* __restrict__ spec_post,
-                              const SegExit* __restrict__ exit_prev, SegExit* __restrict__ exit_next,
-                              SegExit* __restrict__ entry_used, uint32_t* __restrict__ fix_syms,
-                              uint32_t* __restrict__ fix_cnt, uint32_t* __restrict__ conv_idx,
-                              uint32_t* __restrict__ post_flag, uint32_t* __restrict__ changed,
-                              uint32_t sym_stride) {
-  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= nseg_total) return;
+// one fix-up round of segment g: re-parse from the predecessor's exit until the parse meets the
+// speculative one (or the segment ends); *changed counts segments whose exit moved
+__device__ __forceinline__ void parse_fixup_seg(uint32_t g, const LaneDev* __restrict__ lanes,
+                                                const uint32_t* __restrict__ seg_lane, const uint2* __restrict__ prof,
+                                                const uint2* __restrict__ state_map,
+                                                const SegExit* __restrict__ spec_exit,
+                                                const uint32_t* __restrict__ spec_cnt,
+                                                const uint32_t* __restrict__ spec_post,
+                                                const SegExit* exit_prev, SegExit* exit_next,
+                                                SegExit* __restrict__ entry_used, uint32_t* __restrict__ fix_syms,
+                                                uint32_t* __restrict__ fix_cnt, uint32_t* __restrict__ conv_idx,
+                                                uint32_t* __restrict__ post_flag, uint32_t* changed,
+                                                uint32_t sym_stride) {
   const LaneDev Ld = lanes[seg_lane[g]];
   const uint32_t k = g - Ld.seg0;
   if (k == 0) {
@@ -1246,6 +1250,50 @@ __global__ void k_parse_fixup(const LaneDev* __restrict__ lanes, const uint32_t*
   exit_next[g] = ex;
   const SegExit old = exit_prev[g];
   if (old.p != ex.p || old.state != ex.state) atomicAdd(changed, 1u);
+}
+
+__global__ void k_parse_fixup(const LaneDev* __restrict__ lanes, const uint32_t* __restrict__ seg_lane,
+                              uint32_t nseg_total, const uint2* __restrict__ prof,
+                              const uint2* __restrict__ state_map, const SegExit* __restrict__ spec_exit,
+                              const uint32_t* __restrict__ spec_cnt, const uint32_t* __restrict__ spec_post,
+                              const SegExit* __restrict__ exit_prev, SegExit* __restrict__ exit_next,
+                              SegExit* __restrict__ entry_used, uint32_t* __restrict__ fix_syms,
+                              uint32_t* __restrict__ fix_cnt, uint32_t* __restrict__ conv_idx,
+                              uint32_t* __restrict__ post_flag, uint32_t* __restrict__ changed,
+                              uint32_t sym_stride) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nseg_total) return;
+  parse_fixup_seg(g, lanes, seg_lane, prof, state_map, spec_exit, spec_cnt, spec_post, exit_prev, exit_next,
+                  entry_used, fix_syms, fix_cnt, conv_idx, post_flag, changed, sym_stride);
+}
+
+// All fix-up rounds in one cooperative launch: a grid-wide barrier separates the rounds and the
+// loop ends on the device when a round moves no exit -- no host round trip per round.  Three
+// rotating counters: round r counts into c[r % 3]; after its barrier every thread reads it and
+// thread 0 clears c[(r + 2) % 3], whose last reader passed that same barrier.
+__global__ void __launch_bounds__(128) k_parse_fixup_coop(
+    const LaneDev* __restrict__ lanes, const uint32_t* __restrict__ seg_lane, uint32_t nseg_total,
+    const uint2* __restrict__ prof, const uint2* __restrict__ state_map, const SegExit* __restrict__ spec_exit,
+    const uint32_t* __restrict__ spec_cnt, const uint32_t* __restrict__ spec_post, SegExit* exit_a,
+    SegExit* exit_b, SegExit* __restrict__ entry_used, uint32_t* __restrict__ fix_syms,
+    uint32_t* __restrict__ fix_cnt, uint32_t* __restrict__ conv_idx, uint32_t* __restrict__ post_flag,
+    volatile uint32_t* counters, uint32_t sym_stride, uint32_t max_rounds) {
+  cg::grid_group grid = cg::this_grid();
+  const SegExit* cur = exit_a;
+  SegExit* nxt = exit_b;
+  for (uint32_t r = 0; r < max_rounds; r++) {
+    uint32_t* c = const_cast<uint32_t*>(counters) + (r % 3);
+    for (uint64_t g = grid.thread_rank(); g < nseg_total; g += grid.size())
+      parse_fixup_seg((uint32_t)g, lanes, seg_lane, prof, state_map, spec_exit, spec_cnt, spec_post, cur, nxt,
+                      entry_used, fix_syms, fix_cnt, conv_idx, post_flag, c, sym_stride);
+    grid.sync();
+    if (grid.thread_rank() == 0) counters[(r + 2) % 3] = 0;
+    if (counters[r % 3] == 0) return;
+    const SegExit* t = nxt;
+    nxt = const_cast<SegExit*>(cur);
+    cur = t;
+  }
+  if (grid.thread_rank() == 0) counters[3] = 1;  // did not converge within max_rounds
 }
 
 // the fresh state each speculative parse assumed: segment k of a lane starts at k * G with
@@ -2463,24 +2511,56 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_CUDA_TRY(cudaMemcpyAsync(d_post_flag, d_spec_post, 4ull * seg_total, cudaMemcpyDeviceToDevice, st));
   if ((rc = pinned(e, 64 + 16ull * nc))) return rc;
   T.mark("deflate.parse_fixup");
-  SegExit *cur = d_exit_a, *nxt = d_exit_b;
-  // two rounds per host check (a round after convergence only copies the exits): half the syncs
-  for (int round = 0;; round += 2) {
-    BB_CUDA_TRY(cudaMemsetAsync(d_changed, 0, 8, st));
-    for (int r = 0; r < 2; r++) {
-      k_parse_fixup<<<pg, pt, 0, st>>>(d_lanes, d_seg_lane, seg_total, d_prof, d_state_map, d_spec_exit,
-                                       d_spec_cnt, d_spec_post, cur, nxt, d_entry_used, d_fix_syms, d_fix_cnt,
-                                       d_conv_idx, d_post_flag, d_changed + r, sym_stride);
-      BB_LAUNCH_CHECK();
-      std::swap(cur, nxt);
+  {
+    // all rounds in one cooperative launch (BB_FIXUP_HOST=1: one launch per round, host checks)
+    static const bool host_loop = getenv("BB_FIXUP_HOST") != nullptr;
+    int coop_blocks = 0;
+    int dev = 0;
+    BB_CUDA_TRY(cudaGetDevice(&dev));
+    if (!host_loop) {
+      static int per_sm_dev[64] = {};  // occupancy of the cooperative kernel, queried once per device
+      if (dev >= 0 && dev < 64 && per_sm_dev[dev] == 0) {
+        int per_sm = 0;
+        BB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_parse_fixup_coop, 128, 0));
+        per_sm_dev[dev] = std::max(per_sm, 1);
+      }
+      const int per_sm = dev >= 0 && dev < 64 ? per_sm_dev[dev] : 1;
+      coop_blocks = std::min<int>(per_sm * kNumSMs, (int)((seg_total + 127) / 128));
     }
-    BB_CUDA_TRY(cudaMemcpyAsync(e->h_pinned, d_changed + 1, 4, cudaMemcpyDeviceToHost, st));
-    BB_CUDA_TRY(cudaStreamSynchronize(st));
-    uint32_t changed = *reinterpret_cast<uint32_t*>(e->h_pinned);
-    if (changed == 0) break;
-    if (round > (int)seg_total + 2) {
-      set_error("deflate parse fix-up did not converge");
-      return BB_ERROR;
+    if (coop_blocks > 0) {
+      BB_CUDA_TRY(cudaMemsetAsync(d_changed, 0, 16, st));
+      const uint32_t max_rounds = seg_total + 3;
+      uint32_t seg_total_u = seg_total;
+      volatile uint32_t* counters = d_changed;
+      void* args[] = {(void*)&d_lanes, (void*)&d_seg_lane, (void*)&seg_total_u, (void*)&d_prof,
+                      (void*)&d_state_map, (void*)&d_spec_exit, (void*)&d_spec_cnt, (void*)&d_spec_post,
+                      (void*)&d_exit_a, (void*)&d_exit_b, (void*)&d_entry_used, (void*)&d_fix_syms,
+                      (void*)&d_fix_cnt, (void*)&d_conv_idx, (void*)&d_post_flag, (void*)&counters,
+                      (void*)&sym_stride, (void*)&max_rounds};
+      BB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_parse_fixup_coop, dim3(coop_blocks), dim3(128), args,
+                                              0, st));
+      count_launch();
+    } else {
+      BB_CUDA_TRY(cudaMemsetAsync(d_changed, 0, 16, st));  // counters[3]: the coop path's non-convergence flag
+      SegExit *cur = d_exit_a, *nxt = d_exit_b;
+      for (int round = 0;; round += 2) {
+        BB_CUDA_TRY(cudaMemsetAsync(d_changed, 0, 8, st));
+        for (int r = 0; r < 2; r++) {
+          k_parse_fixup<<<pg, pt, 0, st>>>(d_lanes, d_seg_lane, seg_total, d_prof, d_state_map, d_spec_exit,
+                                           d_spec_cnt, d_spec_post, cur, nxt, d_entry_used, d_fix_syms, d_fix_cnt,
+                                           d_conv_idx, d_post_flag, d_changed + r, sym_stride);
+          BB_LAUNCH_CHECK();
+          std::swap(cur, nxt);
+        }
+        BB_CUDA_TRY(cudaMemcpyAsync(e->h_pinned, d_changed + 1, 4, cudaMemcpyDeviceToHost, st));
+        BB_CUDA_TRY(cudaStreamSynchronize(st));
+        uint32_t changed = *reinterpret_cast<uint32_t*>(e->h_pinned);
+        if (changed == 0) break;
+        if (round > (int)seg_total + 2) {
+          set_error("deflate parse fix-up did not converge");
+          return BB_ERROR;
+        }
+      }
     }
   }
   // K6
@@ -2521,8 +2601,14 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_CUDA_TRY(cudaMemcpyAsync(e->h_pinned, d_con_len, 8ull * nc, cudaMemcpyDeviceToHost, st));
   BB_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(e->h_pinned) + 8ull * nc, d_con_status, 4ull * nc,
                               cudaMemcpyDeviceToHost, st));
+  uint32_t* h_nonconv = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(e->h_pinned) + 12ull * nc);
+  BB_CUDA_TRY(cudaMemcpyAsync(h_nonconv, d_changed + 3, 4, cudaMemcpyDeviceToHost, st));
   BB_CUDA_TRY(cudaStreamSynchronize(st));
   T.finish();
+  if (*h_nonconv) {
+    set_error("deflate parse fix-up did not converge");
+    return BB_ERROR;
+  }
   const int* hs = reinterpret_cast<const int*>(reinterpret_cast<char*>(e->h_pinned) + 8ull * nc);
   for (int c = 0; c < nc; c++) {
     container_len[c] = e->h_pinned[c];

@@ -1183,7 +1183,10 @@ __global__ void __launch_bounds__(32 * WD_WARPS, MINB) k_dyn_scan(const PJob* __
   }
 }
 
-__global__ void __launch_bounds__(32 * WD_WARPS) k_dyn_emit(const PJob* __restrict__ jobs, const Chain* __restrict__ chains,
+#ifndef DE_MINB
+#define DE_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * WD_WARPS, DE_MINB) k_dyn_emit(const PJob* __restrict__ jobs, const Chain* __restrict__ chains,
                                                            const uint32_t* __restrict__ chain_nodes,
                                                            const uint32_t* __restrict__ job_of_chain_block,
                                                            const uint32_t* __restrict__ chain_block_base,
