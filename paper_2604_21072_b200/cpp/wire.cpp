@@ -238,6 +238,28 @@ class Arrival {
   bool done_ = false;
 };
 
+// Role threads keep their device contexts until every role thread is done: tearing a context down
+// (bb_ctx_destroy's cudaFree / cudaFreeHost) while other roles still run stalled their next codec
+// call by 0.1-0.4 s (measured on the 1-GPU acceptance-#9 shape).  hold() at the end of a thread's
+// normal path arrives and waits; a thread that unwinds with an error only arrives, so a failing
+// role never blocks the others' shutdown.
+class Linger {
+ public:
+  explicit Linger(Latch& l) : l_(l) {}
+  ~Linger() {
+    if (!done_) l_.arrive();
+  }
+  void hold() {
+    done_ = true;
+    l_.arrive();
+    l_.wait();
+  }
+
+ private:
+  Latch& l_;
+  bool done_ = false;
+};
+
 // make_step_slices' spans (wire.cpp:321-336): elements split into M spans, the
 // first `rem` spans one element longer
 std::vector<std::pair<std::size_t, std::size_t>> step_spans(std::size_t payload_bytes, int micro) {
@@ -799,6 +821,12 @@ std::vector<int> wire_devices(const std::vector<int>& asked) {
 
 double wire_now_ms() { return ms_since_epoch(Clock::now()); }
 
+// BEEPLAN_WIRE_TRACE=1: per-frame timings of the GPU runner's stage workers on stderr
+bool wire_trace() {
+  static const bool on = std::getenv("BEEPLAN_WIRE_TRACE") != nullptr;
+  return on;
+}
+
 Bytes encode_frame(const WireFrame& frame) {
   Bytes out(kFrameHeaderSize + frame.payload.size());
   write_head(out.data(), frame.msg_type, frame.batch_id, frame.micro_index, frame.flags, frame.payload.size());
@@ -1101,6 +1129,8 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
   };
   // source, sink, and per stage its compute and send workers warm up (codec, first peer copy)
   Latch ready(2 + 2 * cfg.stage_count);
+  // threads owning a RoleDevice: sink, source, and per stage its recv / compute / send workers
+  Latch teardown(2 + 3 * cfg.stage_count);
 
   std::vector<std::thread> threads;
   // sink (wire.cpp:543-602): reassemble every step in HBM and compare with the expected stream
@@ -1109,6 +1139,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     try {
       Arrival arrival(ready);
       RoleDevice rd(sink_dev);
+      Linger linger(teardown);
       if (cfg.compress) warm_codec(rd, warm_sample, cfg.backend);
       arrival.now();
       Inbox& in = *inbox.back();
@@ -1179,6 +1210,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
       close_step();
       if (!rep.received.empty())
         rep.metrics.completion_ms = rep.received.back().t_recv_ms - rep.received.front().t_recv_ms;
+      linger.hold();
     } catch (...) {
       role_failed(r);
     }
@@ -1216,6 +1248,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
       std::thread rx([&] {
         try {
           RoleDevice rd(dev);
+          Linger linger(teardown);
           for (;;) {
             double t = 0.0;
             std::optional<DevFrame> f = hop_recv(rd, in, &t);
@@ -1225,6 +1258,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
             inbound.push(*f);
             if (last) break;
           }
+          linger.hold();
         } catch (...) {
           fail_stage();
         }
@@ -1233,6 +1267,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
         try {
           Arrival arrival(ready);
           RoleDevice rd(dev);
+          Linger linger(teardown);
           if (cfg.compress) warm_codec(rd, warm_sample, cfg.backend);
           arrival.now();
           for (;;) {
@@ -1247,7 +1282,9 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
             if (f.head.flags & WireFrame::kFlagCompressed) {
               const double t0 = wire_now_ms();
               const std::size_t need = container_decoded_size(rd, f.payload, f.len);
+              const double t1 = wire_now_ms();
               const int b = pool.take(need + 16);
+              const double t2 = wire_now_ms();
               std::size_t got = 0;
               try {
                 codec_ok(bb_decompress(rd.ctx(), f.payload, f.len, pool.get(b), need, &got, rd.stream()));
@@ -1255,8 +1292,12 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
                 pool.give(b);
                 throw;
               }
+              const double t3 = wire_now_ms();
               rd.sync();
               dec_ms += wire_now_ms() - t0;
+              if (wire_trace())
+                std::fprintf(stderr, "[wire] stage %d dec b%llu m%u: size %.3f take %.3f call %.3f sync %.3f ms\n", r,
+                             (unsigned long long)f.head.batch, f.head.micro, t1 - t0, t2 - t1, t3 - t2, wire_now_ms() - t3);
               drop(f);
               f.inbox_slot = -1;
               f.pool_buf = b;
@@ -1271,6 +1312,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
             if (cfg.compress) {  // compress_out of every relay stage (run_wire_local, wire.cpp:640)
               const double t0 = wire_now_ms();
               const int b = pool.take(bb_compress_bound(f.len, cfg.backend, 1) + 16);
+              const double t1 = wire_now_ms();
               std::size_t len = 0;
               try {
                 codec_ok(bb_compress(rd.ctx(), f.payload, f.len, cfg.backend, 1, pool.get(b),
@@ -1280,6 +1322,9 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
                 throw;
               }
               enc_ms += wire_now_ms() - t0;
+              if (wire_trace())
+                std::fprintf(stderr, "[wire] stage %d enc b%llu m%u: take %.3f call %.3f ms\n", r,
+                             (unsigned long long)f.head.batch, f.head.micro, t1 - t0, wire_now_ms() - t1);
               drop(f);
               f.inbox_slot = -1;
               f.pool_buf = b;
@@ -1289,6 +1334,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
             }
             outbound.push(f);
           }
+          linger.hold();
         } catch (...) {
           fail_stage();
         }
@@ -1297,6 +1343,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
         try {
           Arrival arrival(ready);
           RoleDevice rd(dev);
+          Linger linger(teardown);
           out.warm(rd);
           arrival.now();
           for (;;) {
@@ -1313,6 +1360,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
             if (last) break;
             rep.sent.push_back(rec);
           }
+          linger.hold();
         } catch (...) {
           fail_stage();
         }
@@ -1335,6 +1383,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
     const int r = 0;
     try {
       RoleDevice rd(src_dev);
+      Linger linger(teardown);
       if (cfg.compress) warm_codec(rd, warm_sample, cfg.backend);
       hop.front()->warm(rd);
       ready.arrive();
@@ -1376,6 +1425,7 @@ WireLocalResult run_wire_local(const WireLocalConfig& cfg, const WireLocalOption
       out.send(rd, bye);
       rep.metrics.completion_ms = last_sent - first_offer;
       rep.metrics.step_ms = steps > 0 ? rep.metrics.completion_ms / steps : 0.0;
+      linger.hold();
     } catch (...) {
       role_failed(r);
     }
