@@ -346,3 +346,51 @@ def test_parallel_inflate_checks_the_zlib_header(codec, oracle):
         with pytest.raises(codec.CorruptContainer):
             dec(blob, len(data))
     assert dec(bytes(base), len(data)) == data
+
+
+def test_sequential_inflate_on_large_streams(codec, oracle, monkeypatch):
+    """The exact sequential decoder (the fallback that defines uncompress() status) on streams
+    the parallel path would normally take: CTA-copied stored blocks longer than the 32 KiB window,
+    matches reaching exactly 32768 back through the shared-memory window, mixed block types,
+    and corruption status parity with the oracle."""
+    from oracle.oracle import OracleError
+    dec = codec.backend_by_id(codec.kBackendDeflate).decode
+    monkeypatch.setenv("BB_INFLATE_SEQ", "1")
+    rng = random.Random(31)
+    far = bytearray(rng.choice(b"\x00\x01\x02\x03") for _ in range(32768 + 40000))
+    far[1000:1030] = bytes(rng.randrange(128, 256) for _ in range(30))
+    far[1000 + 32768:1030 + 32768] = far[1000:1030]  # a match exactly 32768 back
+    cases = [random.Random(5).randbytes(300000), oracle.synth_bf16(200000, 3),
+             oracle.synth_fp16(150000, 2)[1::2], b"\x42" * 200000, bytes(far),
+             random.Random(6).randbytes(70000) + b"\x07" * 70000 + random.Random(7).randbytes(70000)]
+    before = _inflate_counts()
+    for data in cases:
+        for level in (0, 1, 6, 9):
+            blob = zlib.compress(data, level)
+            assert dec(blob, len(data)) == data, (len(data), level)
+            assert dec(blob + b"tail", len(data)) == data
+    after = _inflate_counts()
+    assert after[0] == before[0], "BB_INFLATE_SEQ must keep every stream on the sequential decoder"
+    # status parity on corrupted large streams (stored and compressed blocks)
+    for trial in range(24):
+        data = cases[trial % 3]
+        blob = bytearray(zlib.compress(data, (0, 6)[trial % 2]))
+        for _ in range(1 + rng.randrange(4)):
+            blob[rng.randrange(len(blob))] ^= 1 << rng.randrange(8)
+        if trial % 5 == 0:
+            blob = blob[: rng.randrange(len(blob) + 1)]
+        blob = bytes(blob)
+        expected = len(data) if trial % 6 else rng.choice([0, len(data) - 1, len(data) + 1])
+        try:
+            want = oracle.zlib_uncompress(blob, expected)
+            want_ok = len(want) == expected
+        except OracleError:
+            want_ok = False
+        try:
+            got = dec(blob, expected)
+            got_ok = True
+        except codec.CorruptContainer:
+            got_ok = False
+        assert got_ok == want_ok, (trial, expected)
+        if got_ok:
+            assert got == want
