@@ -182,11 +182,16 @@ typedef HTabT<32> HDist;
 
 // inftrees.c rules: over-subscribed -> error; incomplete -> error unless
 // (type != CODES and max length == 1).  type: 0 CODES, 1 LENS, 2 DISTS
-template <int CAP>
-__device__ int htab_build(HTabT<CAP>* t, const uint8_t* lens, int n, int type) {
+template <int CAP, bool ROLLED, class Lens>
+__device__ int htab_build_fn(HTabT<CAP>* t, Lens lens, int n, int type) {
   uint16_t count[16];
   for (int i = 0; i < 16; i++) count[i] = 0;
-  for (int s = 0; s < n; s++) count[lens[s]]++;
+  if constexpr (ROLLED) {
+#pragma unroll 1
+    for (int s = 0; s < n; s++) count[lens(s)]++;
+  } else {
+    for (int s = 0; s < n; s++) count[lens(s)]++;
+  }
   int max = 15;
   while (max >= 1 && count[max] == 0) max--;
   t->max = max;
@@ -212,9 +217,20 @@ __device__ int htab_build(HTabT<CAP>* t, const uint8_t* lens, int n, int type) {
     t->lim[l] = (uint16_t)min((code + count[l]) << (15 - l), 32768u);
     t->base[l] = (int16_t)((int)offs[l] - (int)code);
   }
-  for (int s = 0; s < n; s++)
-    if (lens[s]) t->sym[offs[lens[s]]++] = (uint16_t)s;
+  if constexpr (ROLLED) {
+#pragma unroll 1
+    for (int s = 0; s < n; s++)
+      if (lens(s)) t->sym[offs[lens(s)]++] = (uint16_t)s;
+  } else {
+    for (int s = 0; s < n; s++)
+      if (lens(s)) t->sym[offs[lens(s)]++] = (uint16_t)s;
+  }
   return 0;
+}
+
+template <int CAP>
+__device__ int htab_build(HTabT<CAP>* t, const uint8_t* lens, int n, int type) {
+  return htab_build_fn<CAP, false>(t, [lens](int s) { return (uint32_t)lens[s]; }, n, type);
 }
 
 // limits held in registers while a block is decoded
@@ -255,34 +271,91 @@ struct Tables {
 };
 
 __device__ void static_tables(Tables* T) {
-  uint8_t lens[288];
-  for (int i = 0; i < 288; i++) lens[i] = i < 144 ? 8 : i < 256 ? 9 : i < 280 ? 7 : 8;
-  htab_build(&T->lit, lens, 288, 1);
-  for (int i = 0; i < 30; i++) lens[i] = 5;
-  lens[30] = lens[31] = 5;
-  htab_build(&T->dist, lens, 32, 2);
+  // lengths computed, not stored (no 288-byte array on the stack); loops kept rolled
+  htab_build_fn<288, true>(&T->lit, [](int i) { return i < 144 ? 8u : i < 256 ? 9u : i < 280 ? 7u : 8u; }, 288, 1);
+  htab_build_fn<32, true>(&T->dist, [](int) { return 5u; }, 32, 2);
 }
 
-// Reads a dynamic block header at r (positioned after the 3 header bits).
-__device__ int read_dynamic(BitReader& r, Tables* T) {
-  uint32_t nlen = r.take(5) + 257, ndist = r.take(5) + 1, ncode = r.take(4) + 4;
+// The code-length code (19 symbols, lengths <= 7) held in registers: limit compares for the
+// length, packed per-length bases and a packed sorted-symbol list for the symbol -- no tables in
+// local memory (htab_build's arrays went to the stack of every kernel that parsed a header).
+struct ClCode {
+  uint32_t lim[6];  // left-justified 7-bit limits of lengths 1..6 (a complete code's lim[7] is 128)
+  uint64_t base;    // 8-bit field l: offs[l] - code[l] + 128
+  uint64_t lo, hi;  // symbols in canonical order, 5 bits each: entries 0..11 in lo, 12..18 in hi
+};
+
+// y: the ncode 3-bit lengths in stream order.  inflate_table's CODES rules: over-subscribed or
+// incomplete codes are errors; an empty code (zlib decodes every length as 0, so the block
+// fails on its missing end-of-block code) is rejected here directly.
+__device__ __forceinline__ bool cl_build(ClCode& c, uint64_t y, uint32_t ncode) {
+  constexpr uint8_t slot[19] = {3, 17, 15, 13, 11, 9, 7, 5, 4, 6, 8, 10, 12, 14, 16, 18, 0, 1, 2};
+  uint32_t L[19];
+  uint64_t cnt = 0;  // 8-bit count per length (field l; field 0 collects the unused symbols)
+#pragma unroll
+  for (int s = 0; s < 19; s++) {
+    L[s] = (uint32_t)slot[s] < ncode ? (uint32_t)(y >> (3 * slot[s])) & 7u : 0u;
+    cnt += 1ull << (8 * L[s]);
+  }
+  uint32_t code = 0, offs = 0;
+  int left = 1;
+  uint64_t offp = 0;
+  c.base = 0;
+#pragma unroll
+  for (int l = 1; l <= 7; l++) {
+    const uint32_t k = (uint32_t)(cnt >> (8 * l)) & 0xffu;
+    left = (left << 1) - (int)k;
+    if (left < 0) return false;
+    offp |= (uint64_t)offs << (8 * l);
+    c.base |= (uint64_t)(offs - code + 128u) << (8 * l);
+    if (l <= 6) c.lim[l - 1] = (code + k) << (7 - l);
+    code = (code + k) << 1;
+    offs += k;
+  }
+  if (left != 0) return false;
+  uint64_t run = 0;
+  c.lo = c.hi = 0;
+#pragma unroll
+  for (int s = 0; s < 19; s++) {
+    const uint32_t l = L[s];
+    const uint32_t pos = (uint32_t)((offp + run) >> (8 * l)) & 0xffu;  // fields <= 38: no carries
+    run += 1ull << (8 * l);
+    if (l) {
+      if (pos < 12) c.lo |= (uint64_t)s << (5 * pos);
+      else c.hi |= (uint64_t)s << (5 * (pos - 12));
+    }
+  }
+  return true;
+}
+
+// one code-length symbol from the next stream bits (hold: bit 0 = next bit); len = its length
+__device__ __forceinline__ uint32_t cl_decode(const ClCode& c, uint64_t hold, uint32_t& len) {
+  const uint32_t w = __brev((uint32_t)hold) >> 25;  // next 7 bits, first stream bit most significant
+  uint32_t l = 1;
+#pragma unroll
+  for (int k = 0; k < 6; k++) l += (w >= c.lim[k]);
+  const uint32_t idx = (uint32_t)((c.base >> (8 * l)) & 0xffu) - 128u + (w >> (7 - l));
+  len = l;
+  return idx < 12 ? (uint32_t)(c.lo >> (5 * idx)) & 31u : (uint32_t)(c.hi >> (5 * (idx - 12))) & 31u;
+}
+
+// Dynamic block header at r (after the 3 header bits) up to the code lengths: lens[0, nlen + ndist)
+// receives the literal/length then distance code lengths.  0 ok, -1 invalid (inflate.c TABLE /
+// LENLENS / CODELENS rules, incl. the end-of-block code).
+__device__ int read_code_lengths(BitReader& r, uint8_t* lens, uint32_t& nlen, uint32_t& ndist) {
+  nlen = r.take(5) + 257, ndist = r.take(5) + 1;
+  const uint32_t ncode = r.take(4) + 4;
   if (nlen > 286 || ndist > 30) return -1;
-  uint8_t lens[320];
-  for (int i = 0; i < 19; i++) lens[i] = 0;
-  for (uint32_t i = 0; i < ncode; i++) lens[p_order[i]] = (uint8_t)r.take(3);
-  if (r.past_end()) return -1;
-  HDist* ch = &T->dist;  // scratch for the code-length code
-  if (htab_build(ch, lens, 19, 0)) return -1;
+  ClCode ch;
+  const uint64_t y = peek64(r.p, r.n, r.pos) & ((1ull << (3 * ncode)) - 1);
+  r.init(r.p, r.n, r.pos + 3 * ncode);
+  if (r.past_end() || !cl_build(ch, y, ncode)) return -1;
   uint32_t have = 0;
   while (have < nlen + ndist) {
-    int sym;
-    if (ch->max == 0) {
-      r.take(1);
-      sym = 0;
-    } else {
-      sym = hdecode(r, ch);
-      if (sym < 0) return -1;
-    }
+    r.refill();
+    uint32_t l;
+    const uint32_t sym = cl_decode(ch, r.hold, l);
+    r.drop(l);
     if (sym < 16) {
       lens[have++] = (uint8_t)sym;
     } else {
@@ -302,8 +375,78 @@ __device__ int read_dynamic(BitReader& r, Tables* T) {
     if (r.past_end()) return -1;
   }
   if (lens[256] == 0) return -1;
+  return 0;
+}
+
+// Reads a dynamic block header at r (positioned after the 3 header bits); one thread.
+__device__ int read_dynamic(BitReader& r, Tables* T) {
+  uint8_t lens[320];
+  uint32_t nlen, ndist;
+  if (read_code_lengths(r, lens, nlen, ndist)) return -1;
   if (htab_build(&T->lit, lens, nlen, 1)) return -1;
   if (htab_build(&T->dist, lens + nlen, ndist, 2)) return -1;
+  return 0;
+}
+
+// htab_build by a whole warp: lens[0, n) in shared memory, cnt = 16 words of shared scratch.
+// Counts and in-length ranks by __match_any_sync per 32 symbols, the limits / bases as a lane scan
+// over the lengths, the sorted symbols placed in parallel.  Same tables and return value as
+// htab_build (inftrees.c rules).
+template <int CAP>
+__device__ int warp_htab_build(HTabT<CAP>* t, const uint8_t* lens, int n, int type, int lane, uint32_t* cnt) {
+  constexpr int NC = (CAP + 31) / 32;
+  if (lane < 16) cnt[lane] = 0;
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1;
+  uint32_t rank[NC];
+#pragma unroll
+  for (int c = 0; c < NC; c++) {
+    const int sidx = 32 * c + lane;
+    const uint32_t l = sidx < n ? lens[sidx] : 0u;
+    const unsigned m = __match_any_sync(0xffffffffu, l);
+    const uint32_t before = cnt[l];
+    rank[c] = before + __popc(m & lt);
+    __syncwarp();
+    if ((m & lt) == 0) cnt[l] = before + __popc(m);
+    __syncwarp();
+  }
+  const uint32_t k = (lane >= 1 && lane <= 15) ? cnt[lane] : 0u;
+  const unsigned nz = __ballot_sync(0xffffffffu, k != 0);
+  const int max = nz ? 31 - __clz(nz) : 0;
+  // inclusive scans over lengths: left-justified limits (sum of count[j] << (15 - j)) and offsets
+  uint32_t lim = (lane >= 1 && lane <= 15) ? k << (15 - lane) : 0u, offs = k;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, lim, o), b = __shfl_up_sync(0xffffffffu, offs, o);
+    if (lane >= o) lim += a, offs += b;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, lim, 15);
+  if (max == 0) {
+    if (lane < 16) t->lim[lane] = 0;
+    if (lane == 0) t->max = 0;
+    __syncwarp();
+    return 0;
+  }
+  if (total > 32768u) return -1;                              // over-subscribed
+  if (total < 32768u && (type == 0 || max != 1)) return -1;  // incomplete
+  const uint32_t excl_lim = lim - ((lane >= 1 && lane <= 15) ? k << (15 - lane) : 0u);
+  const uint32_t excl_off = offs - k;
+  __syncwarp();
+  if (lane >= 1 && lane <= 15) {
+    const uint32_t code = excl_lim >> (15 - lane);
+    t->lim[lane] = (uint16_t)min(lim, 32768u);
+    t->base[lane] = (int16_t)((int)excl_off - (int)code);
+    cnt[lane] = excl_off;
+  }
+  if (lane == 0) t->max = max;
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < NC; c++) {
+    const int sidx = 32 * c + lane;
+    const uint32_t l = sidx < n ? lens[sidx] : 0u;
+    if (l) t->sym[cnt[l] + rank[c]] = (uint16_t)sidx;
+  }
+  __syncwarp();
   return 0;
 }
 
@@ -355,19 +498,19 @@ __device__ bool verify_dynamic(const uint8_t* p, uint64_t n, uint64_t b) {
   r.init(p, n, b + 3);
   uint32_t nlen = r.take(5) + 257, ndist = r.take(5) + 1, ncode = r.take(4) + 4;
   if (nlen > 286 || ndist > 30) return false;
-  uint8_t cl[19];
-  for (int i = 0; i < 19; i++) cl[i] = 0;
-  for (uint32_t i = 0; i < ncode; i++) cl[p_order[i]] = (uint8_t)r.take(3);
-  HTabT<19> ch;
-  if (htab_build(&ch, cl, 19, 0) || ch.max == 0) return false;
-  Lims L;
-  L.load(&ch);
+  ClCode ch;
+  const uint64_t y = peek64(p, n, r.pos) & ((1ull << (3 * ncode)) - 1);
+  r.init(p, n, r.pos + 3 * ncode);
+  if (!cl_build(ch, y, ncode)) return false;
   uint32_t have = 0, prev = 0, kl = 0, kd = 0;
   uint16_t cnt1l = 0, cnt1d = 0, maxl = 0, maxd = 0;
   bool eob = false;
   while (have < nlen + ndist) {
-    int sym = hdecode(r, &ch, L);
-    if (sym < 0) return false;
+    r.refill();
+    uint32_t cl;
+    const uint32_t sym = cl_decode(ch, r.hold, cl);
+    r.drop(cl);
+    if (r.past_end()) return false;
     uint32_t len, copy;
     if (sym < 16) {
       len = (uint32_t)sym;
@@ -538,7 +681,13 @@ __global__ void k_candidates4(const PJob* __restrict__ jobs, const uint64_t* __r
   if ((lane & 7) == 0 && B0 < J.n + 32) sbm[J.sbm + (B0 >> 5)] = wv;
 }
 
-__global__ void k_verify_dynamic(const PJob* __restrict__ jobs, const uint64_t* __restrict__ surv,
+#ifndef VD_THREADS
+#define VD_THREADS 256
+#endif
+#ifndef VD_MINB
+#define VD_MINB 4  // 64 registers (small spills): occupancy over the survivors' divergent walks
+#endif
+__global__ void __launch_bounds__(VD_THREADS, VD_MINB) k_verify_dynamic(const PJob* __restrict__ jobs, const uint64_t* __restrict__ surv,
                                  const unsigned long long* __restrict__ surv_cnt, uint64_t surv_cap,
                                  uint32_t* __restrict__ dbm, uint32_t* __restrict__ fail, int njobs) {
   const uint64_t cnt = *surv_cnt;
@@ -903,13 +1052,14 @@ struct WarpSm {
 };
 
 // Two register budgets: MINB 5 (127 registers, no spills) has the shortest latency per block
-// (config1's few blocks: 0.39 vs 0.48 ms with the other); MINB 16 (64 registers, small spills)
-// has 3x the resident warps and the best throughput over many blocks (config2: 3.53 vs 3.82 ms).
+// (config1's few blocks: 0.39 vs 0.48 ms with the other); MINB 12 (85 registers) has 2.4x the
+// resident warps and the best throughput over many blocks (config2: 3.46 ms; MINB 16 3.51,
+// MINB 10 3.70, MINB 5 3.82).
 #ifndef DS_MINB
 #define DS_MINB 5
 #endif
 #ifndef DS_MINB_WIDE
-#define DS_MINB_WIDE 16
+#define DS_MINB_WIDE 12
 #endif
 template <int MINB>
 __global__ void __launch_bounds__(32 * WD_WARPS, MINB) k_dyn_scan(const PJob* __restrict__ jobs,
@@ -931,17 +1081,27 @@ __global__ void __launch_bounds__(32 * WD_WARPS, MINB) k_dyn_scan(const PJob* __
   uint64_t d0 = 0;
   int rc = 0;
   bool final_blk = false;
+  // code lengths (lane 0, register-resident code-length code) into shared scratch -- the record
+  // arrays, written only from round 1 on -- then both tables built by the whole warp
+  uint8_t* lens = reinterpret_cast<uint8_t*>(&W.rpos[0][0]);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(lens + 320);
+  uint32_t nlen = 0, ndist = 0;
   if (lane == 0) {
     BitReader r;
     r.init(J.src, J.n, nd.start);
     uint32_t hdr = r.take(3);
     final_blk = hdr & 1;
-    rc = read_dynamic(r, &W.T);
+    rc = read_code_lengths(r, lens, nlen, ndist);
     d0 = r.pos;
   }
   rc = __shfl_sync(0xffffffffu, rc, 0);
   d0 = __shfl_sync(0xffffffffu, d0, 0);
   final_blk = __shfl_sync(0xffffffffu, (int)final_blk, 0);
+  nlen = __shfl_sync(0xffffffffu, nlen, 0);
+  ndist = __shfl_sync(0xffffffffu, ndist, 0);
+  __syncwarp();
+  if (!rc) rc = warp_htab_build(&W.T.lit, lens, (int)nlen, 1, lane, cnt);
+  if (!rc) rc = warp_htab_build(&W.T.dist, lens + nlen, (int)ndist, 2, lane, cnt);
   if (rc) {
     if (lane == 0) {
       nd.flags = 8;  // dynamic, not ok
@@ -2106,9 +2266,6 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
     T.mark("inflate.verify_headers");
 #ifndef VD_GRID_MUL
 #define VD_GRID_MUL 8
-#endif
-#ifndef VD_THREADS
-#define VD_THREADS 256
 #endif
     k_verify_dynamic<<<kNumSMs * VD_GRID_MUL, VD_THREADS, 0, st>>>(d_jobs, d_surv, d_surv_cnt, surv_cap, d_dbm, d_fail, nj);
     BB_LAUNCH_CHECK();
