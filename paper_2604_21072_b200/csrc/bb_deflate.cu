@@ -800,6 +800,427 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
 }
 
 // ---------------------------------------------------------------------------
+// K4G (default): the chain walk restricted to the candidates that can matter.
+//
+// longest_match() returns the first candidate of maximal length among the first B
+// (32 or 128) entries of p's hash chain.  A candidate can replace best only if its
+// match is longer, i.e. it shares p's first best + 1 bytes; once best >= 3 every
+// such candidate shares p's 4-gram.  And two positions with the same 4-gram have
+// the same hash, so the same-4-gram positions before p form a subsequence of p's
+// chain, and for any candidate c on it the rest of that subsequence is c's own.
+// K4G therefore splits the walk in two exact passes:
+//
+//   k_gram4     per position x, walking x's zlib chain (K3 links): the first
+//               candidate sharing x's 3-gram and the first sharing its 4-gram, each
+//               with its chain step number (budget 128, the MAX_DIST rules of the
+//               head and of later entries).  On bf16 exponent planes ~17 steps
+//               instead of ~108.
+//   k_profile4  per position p: the first same-3-gram candidate (the only one that
+//               matters while best < 4, i.e. a match of exactly 3), then the
+//               same-4-gram subsequence, hopping link to link and adding the step
+//               counts so the budget (32 snapshot, 128) and the distance limit are
+//               applied exactly as the full walk applies them; quick reject on bytes
+//               (best - 1, best), extension, nice_match, first maximum.  ~11 hops.
+//
+// Profiles are bit-identical to K4's (tests compare both with the oracle's
+// orc_match_profile and the full-size goldens).
+//
+// g3[x]: d3 (15 bits, 0 = none) | s3 << 15 (8 bits) | head-at-MAX_DIST << 23 | live << 24
+// g4[x]: d4 (15 bits, 0 = none) | s4 << 15 (8 bits)
+constexpr uint32_t G3_FLAG = 1u << 23, G3_LIVE = 1u << 24;
+constexpr uint32_t PF2_SEG = 12288;  // k_profile4 positions per CTA
+constexpr uint32_t PF2_WIN = WSIZE + PF2_SEG + MAX_MATCH + 32;
+constexpr uint32_t PF2_SMEM = 5 * PF2_WIN;  // u32 words (link4 index | bytes q, q+1) + u8 step counts
+
+// K4's window staging: w32[i + 1] = 1-based index of the previous same-hash position
+// (0 = none) | bytes (q, q+1) << 16 for window position q = wlo + i
+__device__ __forceinline__ void pf_stage_links(uint32_t* w32, const uint8_t* src, const uint16_t* pdl, uint64_t n,
+                                               uint64_t wlo, uint64_t e, uint32_t wlen) {
+  if (threadIdx.x == 0) w32[0] = 0;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(pdl)) & 7) == 0;
+  const uint32_t nq = (wlen + 3) / 4;
+  uint32_t jf = 0;
+  if (aligned) {
+    const uint64_t lim = umin64(e >= 4 ? e - 4 : 0, n >= 8 ? n - 8 : 0);
+    jf = lim >= wlo ? (uint32_t)umin64((lim - wlo) / 4 + 1, nq) : 0;
+  }
+  constexpr int U = 4;
+  for (uint32_t j0 = threadIdx.x; j0 < jf; j0 += U * blockDim.x) {
+    uint2 l4[U];
+    uint32_t b0[U], b1[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t j = j0 + u * blockDim.x;
+      if (j < jf) {
+        const uint64_t q0 = wlo + 4 * j;
+        l4[u] = __ldg(reinterpret_cast<const uint2*>(pdl + q0));
+        b0[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0));
+        b1[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0 + 4));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t j = j0 + u * blockDim.x;
+      if (j < jf) {
+        const uint32_t i0 = 4 * j;
+        const uint32_t ls[4] = {l4[u].x & 0xffff, l4[u].x >> 16, l4[u].y & 0xffff, l4[u].y >> 16};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const uint32_t i = i0 + k, l = ls[k];
+          uint32_t v = (l && l <= i) ? i - l + 1 : 0;
+          v |= __byte_perm(b0[u], b1[u], (k | ((k + 1) << 4)) & 0xff) << 16;
+          w32[i + 1] = v;
+        }
+      }
+    }
+  }
+  for (uint32_t j = jf + threadIdx.x; j < nq; j += blockDim.x) {
+    const uint32_t i0 = 4 * j;
+    for (uint32_t i = i0; i < i0 + 4 && i < wlen; i++) {
+      const uint64_t q = wlo + i;
+      uint32_t v = 0;
+      if (q < e) {
+        const uint32_t l = pdl[q];
+        if (l && l <= i) v = i - l + 1;
+      }
+      if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
+      if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
+      w32[i + 1] = v;
+    }
+  }
+}
+
+// Lock-step batches with refill: each warp owns a contiguous run of positions; a lane
+// walks one position's chain, GB steps per batch, and lanes whose walk ended take the
+// warp's next positions at the batch boundary (ballot + rank), so the walks' different
+// lengths cost at most one partial batch each instead of diverging the whole warp.
+#ifndef GB_STEPS
+#define GB_STEPS 8
+#endif
+#ifndef PB_STEPS
+#define PB_STEPS 8
+#endif
+__device__ __forceinline__ void warp_range(uint64_t s, uint64_t e, uint64_t& qn, uint64_t& qe) {
+  const uint32_t nw = blockDim.x >> 5, wid = threadIdx.x >> 5;
+  const uint64_t per = (e - s + nw - 1) / nw;
+  qn = umin64(s + wid * per, e);
+  qe = umin64(qn + per, e);
+}
+
+__global__ void __launch_bounds__(PF_THREADS, 1) k_gram4(const LaneDev* __restrict__ lanes,
+                                                         const WorkItem* __restrict__ work,
+                                                         const uint16_t* __restrict__ pd, uint32_t* __restrict__ g3,
+                                                         uint32_t* __restrict__ g4) {
+  extern __shared__ __align__(16) uint32_t w32[];
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + PF_SEG, n);
+  const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
+  const uint32_t wlen = (uint32_t)(e - wlo) + 16;
+  pf_stage_links(w32, L.src, pd + L.pbase, n, wlo, e, wlen);
+  __syncthreads();
+  uint32_t* G3 = g3 + L.pbase;
+  uint32_t* G4 = g4 + L.pbase;
+  const unsigned lt = (1u << (threadIdx.x & 31)) - 1;
+  uint64_t qn, qe;
+  warp_range(s, e, qn, qe);
+  const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w32);
+  uint64_t p = 0;
+  bool has = false, done = true, found4 = false, four = false;
+  // lane state: cb = shared byte address of the current candidate's word; a lane without a
+  // walk sits on the sentinel word 0 with done set
+  uint32_t ix = 0, key = 0, cb = sw, stp = 0, limb = sw, f3c = 0, f3s = 0, hd = 0;
+  for (;;) {
+    // refill (once per batch): idle lanes take the warp's next positions in order
+    const unsigned need = __ballot_sync(0xffffffffu, !has);
+    if (need && qn < qe) {
+      const uint64_t myp = qn + __popc(need & lt);
+      qn = umin64(qn + __popc(need), qe);
+      if (!has && myp < qe) {
+        p = myp;
+        ix = (uint32_t)(p - wlo) + 1;
+        const uint32_t wp = w32[ix];
+        const uint32_t c0 = wp & 0xffff, d0 = ix - c0;
+        if (p + MIN_MATCH <= n && c0 != 0 && d0 <= MAX_DIST && wlo + c0 - 1 != 0) {
+          const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
+          limb = sw + 4 * (limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0u);
+          hd = G3_LIVE | (d0 == MAX_DIST ? G3_FLAG : 0u);
+          four = p + 4 <= n;
+          key = __byte_perm(wp, w32[ix + 2], 0x7632);  // bytes p .. p + 3
+          cb = sw + 4 * c0;
+          stp = 1;
+          f3c = f3s = 0;
+          found4 = false;
+          has = true;
+          done = false;
+        } else {
+          G3[p] = 0;
+          G4[p] = 0;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, has)) {
+      if (qn >= qe) break;
+      continue;
+    }
+    // GB chain steps, branch-free; a lane whose walk ended stays on its last candidate
+#pragma unroll
+    for (int t = 0; t < GB_STEPS; t++) {
+      uint32_t wc, wc2;
+      asm("ld.shared.u32 %0, [%1];" : "=r"(wc) : "r"(cb));
+      asm("ld.shared.u32 %0, [%1+8];" : "=r"(wc2) : "r"(cb));
+      const uint32_t m = __byte_perm(wc, wc2, 0x7632) ^ key;  // candidate bytes 0..3 vs the position's
+      const bool h3 = !done && (m & 0xffffffu) == 0;
+      const bool first3 = h3 && f3s == 0;
+      f3c = first3 ? cb : f3c;
+      f3s = first3 ? stp : f3s;
+      const bool h4 = h3 && four && m == 0;
+      found4 = found4 || h4;
+      const uint32_t nb = sw + ((wc & 0xffffu) << 2);  // entries after the head must lie above the limit
+      const bool end = h4 || stp >= MAX_CHAIN || nb <= limb;
+      const bool adv = !done && !end;
+      done = done || end;
+      cb = adv ? nb : cb;
+      stp = adv ? stp + 1 : stp;
+    }
+    if (has && done) {
+      G3[p] = f3s ? (ix - ((f3c - sw) >> 2)) | (f3s << 15) | hd : hd;
+      G4[p] = found4 ? (ix - ((cb - sw) >> 2)) | (stp << 15) : 0u;
+      has = false;
+    }
+  }
+}
+
+// K4G second pass: one CTA per PF2_SEG positions.  Window word: 1-based index of the
+// previous same-4-gram position (0 = none or outside the window) | bytes (q, q+1) << 16,
+// plus the zlib step count of that hop in a byte array behind the words.  A lane's
+// candidates are the first same-3-gram one, then the 4-gram hops.  As in K4, a batch of
+// PB_STEPS candidates is walked branch-free and only records which pass the quick test
+// (bytes best - 1, best against a best that may lag by one batch); the recorded ones
+// are then extended in chain order.  Lanes refill at batch boundaries.
+__global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __restrict__ lanes,
+                                                            const WorkItem* __restrict__ work,
+                                                            const uint32_t* __restrict__ g3,
+                                                            const uint32_t* __restrict__ g4, uint2* __restrict__ prof,
+                                                            int with_bytes) {
+  extern __shared__ __align__(16) uint32_t w32[];
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + PF2_SEG, n);
+  const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
+  const uint32_t wlen = (uint32_t)(e - wlo) + MAX_MATCH + 16;  // <= PF2_WIN - 1
+  uint8_t* sk = reinterpret_cast<uint8_t*>(w32 + PF2_WIN);
+  const uint8_t* src = L.src;
+  const uint32_t* G4 = g4 + L.pbase;
+  const uint32_t* G3 = g3 + L.pbase;
+  if (threadIdx.x == 0) w32[0] = 0, sk[0] = 0;
+  {
+    // four window positions per thread and step: one 16-byte load of their g4 records, two
+    // 4-byte loads of their bytes (wlo, the lane bases and the arrays are 4-aligned)
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 3) | (reinterpret_cast<uintptr_t>(G4) & 15)) == 0;
+    const uint32_t nq = (wlen + 3) / 4;
+    uint32_t jf = 0;
+    if (aligned) {
+      const uint64_t lim = umin64(e >= 4 ? e - 4 : 0, n >= 8 ? n - 8 : 0);
+      jf = lim >= wlo ? (uint32_t)umin64((lim - wlo) / 4 + 1, nq) : 0;
+    }
+    constexpr int U = 4;
+    for (uint32_t j0 = threadIdx.x; j0 < jf; j0 += U * blockDim.x) {
+      uint4 gv[U];
+      uint32_t b0[U], b1[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j < jf) {
+          const uint64_t q0 = wlo + 4 * j;
+          gv[u] = __ldg(reinterpret_cast<const uint4*>(G4 + q0));
+          b0[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0));
+          b1[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0 + 4));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j < jf) {
+          const uint32_t i0 = 4 * j;
+          const uint32_t gs[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+          uint32_t kk = 0;
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const uint32_t i = i0 + k, g = gs[k], d = g & 0x7fff;
+            const bool in = d && d <= i;
+            w32[i + 1] = (in ? i - d + 1 : 0u) | (__byte_perm(b0[u], b1[u], (k | ((k + 1) << 4)) & 0xff) << 16);
+            kk |= (in ? g >> 15 : 0u) << (8 * k);
+          }
+          // bytes i0 + 1 .. i0 + 4 of sk: two aligned 16-bit stores are not possible at odd
+          // offsets, so four byte stores
+#pragma unroll
+          for (int k = 0; k < 4; k++) sk[i0 + k + 1] = (uint8_t)(kk >> (8 * k));
+        }
+      }
+    }
+    for (uint32_t j = jf + threadIdx.x; j < nq; j += blockDim.x) {
+      for (uint32_t i = 4 * j; i < 4 * j + 4 && i < wlen; i++) {
+        const uint64_t q = wlo + i;
+        uint32_t v = 0, k = 0;
+        if (q < e) {
+          const uint32_t g = __ldg(G4 + q), d = g & 0x7fff;
+          if (d && d <= i) v = i - d + 1, k = g >> 15;
+        }
+        if (q < n) v |= (uint32_t)__ldg(src + q) << 16;
+        if (q + 1 < n) v |= (uint32_t)__ldg(src + q + 1) << 24;
+        w32[i + 1] = v;
+        sk[i + 1] = (uint8_t)k;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w32);
+  const uint32_t skb = sw + 4 * PF2_WIN;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  uint64_t qn, qe;
+  warp_range(s, e, qn, qe);
+  // the warp's next 32 positions' g3 records, one per lane, loaded a batch ahead
+  uint32_t gbuf = qn + lane < qe ? __ldg(G3 + qn + lane) : 0u;
+  uint64_t p = 0;
+  bool has = false, done = true, snap = false;
+  uint32_t ip1 = 0, maxl = 0, nice = 0, lim1 = 0, flag = 0, best = MIN_MATCH - 1, bestd = 0, r32 = 0;
+  uint32_t key = 0;  // bytes (best - 1, best) of p (best >= 4 while a lane walks)
+  uint32_t c = 0, stp = 0;
+  auto store = [&](bool live) {
+    const uint32_t yb = with_bytes ? (w32[ip1 - 1] << 8) & 0xff000000u : (live ? flag : 0u);
+    if (live && !snap) r32 = prof_pack(best, bestd);
+    prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
+  };
+  // match length of candidate cx whose first `from` (>= 4) bytes are known to match p's
+  auto extend = [&](uint32_t cx, uint32_t from) {
+    uint32_t len = from;
+    while (len < maxl) {
+      const uint32_t x = (w32[cx + len] ^ w32[ip1 + len]) >> 16;
+      if (x) {
+        len += (x & 0xff) == 0;
+        break;
+      }
+      len += 2;
+    }
+    return min(len, maxl);
+  };
+  for (;;) {
+    const unsigned need = __ballot_sync(0xffffffffu, !has);
+    if (need && qn < qe) {
+      const uint32_t cnt = __popc(need), r = __popc(need & lt);
+      const uint32_t gg = __shfl_sync(0xffffffffu, gbuf, r & 31);
+      const uint64_t myp = qn + r;
+      // the buffer moves on by cnt positions; the lanes past its end load new records
+      const uint32_t moved = __shfl_down_sync(0xffffffffu, gbuf, cnt & 31);
+      const uint64_t qn2 = umin64(qn + cnt, qe);
+      gbuf = lane + cnt < 32 ? moved : (qn2 + lane < qe ? __ldg(G3 + qn2 + lane) : 0u);
+      if (!has && myp < qe) {
+        p = myp;
+        ip1 = (uint32_t)(p - wlo) + 1;
+        const uint32_t d3 = gg & 0x7fff;
+        flag = gg & G3_FLAG ? PROF_AT_MAXDIST : 0u;
+        best = MIN_MATCH - 1, bestd = 0, r32 = 0, snap = false;
+        bool walk = false;
+        if (d3) {  // live, with a same-3-gram candidate within the budget
+          const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
+          nice = min(NICE_LENGTH, la), maxl = min(MAX_MATCH, la);
+          const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
+          lim1 = limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0;
+          // the first same-3-gram candidate (the only source of a match of exactly 3)
+          const uint32_t c3 = ip1 - d3, s3 = (gg >> 15) & 0xff;
+          if (s3 > 32) snap = true;  // r32 stays "no match"
+          best = (w32[c3 + 2] ^ w32[ip1 + 2]) >> 16 ? 3u : 4u;  // byte 3
+          if (best == 4) best = extend(c3, 4);
+          best = min(best, maxl);
+          bestd = d3;
+          // then the first same-4-gram candidate (it matches >= 4 > 3, so it is extended at once)
+          const uint32_t c4 = w32[ip1] & 0xffff, s4 = sk[ip1];
+          if (best < nice && best < maxl && c4 != 0 && s4 <= MAX_CHAIN && (c4 > lim1 || (s4 == 1 && c4 == lim1))) {
+            if (c4 != c3) {
+              if (s4 > 32 && !snap) {
+                r32 = prof_pack(best, bestd);
+                snap = true;
+              }
+              const uint32_t len = extend(c4, 4);
+              if (len > best) best = len, bestd = ip1 - c4;
+            }
+            c = w32[c4] & 0xffff;
+            stp = s4 + sk[c4];
+            walk = best < nice && best < maxl && c != 0 && stp <= MAX_CHAIN && c > lim1;
+          }
+        }
+        if (walk) {
+          key = w32[ip1 + best - 1] >> 16;
+          has = true;
+          done = false;
+        } else {
+          store((gg & G3_LIVE) != 0);
+        }
+      }
+      qn = qn2;
+    }
+    if (!__any_sync(0xffffffffu, has)) {
+      if (qn >= qe) break;
+      continue;
+    }
+    // PB_STEPS hops along the 4-gram subsequence, branch-free; candidates passing the quick
+    // test (bytes best - 1, best of the lagging best) are recorded
+    uint32_t cand[PB_STEPS], cst[PB_STEPS];
+    uint32_t mask = 0;
+    const uint32_t qb = sw + 4 * best - 2;  // + 4 c: the candidate's bytes (best - 1, best)
+#pragma unroll
+    for (int t = 0; t < PB_STEPS; t++) {
+      uint32_t wc, we, k;
+      asm("ld.shared.u32 %0, [%1];" : "=r"(wc) : "r"(sw + 4 * c));
+      asm("ld.shared.u16 %0, [%1];" : "=r"(we) : "r"(qb + 4 * c));
+      asm("ld.shared.u8 %0, [%1];" : "=r"(k) : "r"(skb + c));
+      cand[t] = c;
+      cst[t] = stp;
+      mask |= (!done && we == key) ? 1u << t : 0u;
+      const uint32_t nc = wc & 0xffff, ns = stp + k;
+      const bool adv = !done && nc > lim1 && ns <= MAX_CHAIN;
+      done = !adv;
+      c = adv ? nc : c;
+      stp = adv ? ns : stp;
+    }
+    // extend the recorded candidates in chain order
+    bool improved = false;
+    while (mask) {
+      const int t = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t cx = pf_pick(cand, t), sc = pf_pick(cst, t);
+      if (sc > 32 && !snap) {  // the budget-32 result: everything before this candidate
+        r32 = prof_pack(best, bestd);
+        snap = true;
+      }
+      // re-test against the current best if it grew in this flush
+      if (improved && (w32[cx + best - 1] >> 16) != (w32[ip1 + best - 1] >> 16)) continue;
+      const uint32_t len = extend(cx, 4);
+      if (len > best) {
+        best = len;
+        bestd = ip1 - cx;
+        improved = true;
+        if (best >= nice || best >= maxl) {
+          done = true;
+          mask = 0;
+        }
+      }
+    }
+    if (improved) key = w32[ip1 + best - 1] >> 16;
+    if (has && done) {
+      store(true);
+      has = false;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3S + K4S: match profiles over BUCKET-SORTED chains (variant, BB_K4_SORTED=1).
 //
 // zlib's hash chain of position p is the list of earlier positions with the same
@@ -2339,6 +2760,8 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev7, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_gram4, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
+    BB_CUDA_TRY(cudaFuncSetAttribute(k_profile4, cudaFuncAttributeMaxDynamicSharedMemorySize, PF2_SMEM + 16));
     e->tables_ready = true;
   }
   const int nl = (int)jobs.size();
@@ -2357,7 +2780,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     C[c] = ContainerDev{containers[c].dst, containers[c].cap, containers[c].element_count,
                         containers[c].split, -1};
   }
-  std::vector<WorkItem> hp_work, pf_work, ad_work;
+  std::vector<WorkItem> hp_work, pf_work, pf2_work, ad_work;
   std::vector<uint32_t> seg_lane, blk_lane, ad_chunk0(nl);
   uint64_t pos_total = 0, sym_total = 0;
   uint32_t seg_total = 0, blk_total = 0;
@@ -2390,6 +2813,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     L[i] = d;
     for (uint64_t s = 0; s < j.n; s += HP_SEG) hp_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
     for (uint64_t s = 0; s < j.n; s += PF_SEG) pf_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
+    for (uint64_t s = 0; s < j.n; s += PF2_SEG) pf2_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
     ad_chunk0[i] = (uint32_t)ad_work.size();
     for (uint64_t s = 0; s * AD_CHUNK < j.n; s++) ad_work.push_back(WorkItem{(uint32_t)i, (uint32_t)s});
     for (uint32_t k = 0; k < d.nseg; k++) seg_lane.push_back((uint32_t)i);
@@ -2408,7 +2832,8 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t need = 0;
   need += al(sizeof(LaneDev) * nl) + al(sizeof(ContainerDev) * nc);
-  need += al(sizeof(WorkItem) * (hp_work.size() + pf_work.size() + ad_work.size() + 3));
+  need += al(sizeof(WorkItem) * (hp_work.size() + pf_work.size() + pf2_work.size() + ad_work.size() + 4));
+  need += 2 * al(4 * pos_total);  // K4G's g3 / g4
   need += al(4 * seg_lane.size()) + al(4 * blk_lane.size()) + al(4 * nl);
   need += al(2 * pos_total) + al(8 * pos_total);
   need += 2 * al(4ull * seg_total * sym_stride);            // spec + fixup symbols
@@ -2426,6 +2851,9 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   ContainerDev* d_cons = W.take<ContainerDev>(nc);
   WorkItem* d_hp = W.take<WorkItem>(hp_work.size() + 1);
   WorkItem* d_pf = W.take<WorkItem>(pf_work.size() + 1);
+  WorkItem* d_pf2 = W.take<WorkItem>(pf2_work.size() + 1);
+  uint32_t* d_g3 = W.take<uint32_t>(pos_total);
+  uint32_t* d_g4 = W.take<uint32_t>(pos_total);
   WorkItem* d_ad = W.take<WorkItem>(ad_work.size() + 1);
   uint32_t* d_seg_lane = W.take<uint32_t>(seg_lane.size());
   uint32_t* d_blk_lane = W.take<uint32_t>(blk_lane.size());
@@ -2467,6 +2895,9 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     BB_CUDA_TRY(cudaMemcpyAsync(d_hp, hp_work.data(), sizeof(WorkItem) * hp_work.size(), cudaMemcpyHostToDevice, st));
   if (!pf_work.empty())
     BB_CUDA_TRY(cudaMemcpyAsync(d_pf, pf_work.data(), sizeof(WorkItem) * pf_work.size(), cudaMemcpyHostToDevice, st));
+  if (!pf2_work.empty())
+    BB_CUDA_TRY(
+        cudaMemcpyAsync(d_pf2, pf2_work.data(), sizeof(WorkItem) * pf2_work.size(), cudaMemcpyHostToDevice, st));
   if (!ad_work.empty())
     BB_CUDA_TRY(cudaMemcpyAsync(d_ad, ad_work.data(), sizeof(WorkItem) * ad_work.size(), cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_seg_lane, seg_lane.data(), 4 * seg_lane.size(), cudaMemcpyHostToDevice, st));
@@ -2484,9 +2915,19 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
       rc = hash_prev_two_phase(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
       if (rc) return rc;
     }
-    T.mark("deflate.profile");
-    if (!pf_work.empty()) {
+    // K4G (default): first 3- / 4-gram candidates, then the 4-gram subsequence walk;
+    // BB_K4_CLASSIC=1: K4's full lock-step chain walk (bit-identical, 35 ms on config2)
+    static const bool k4_classic = getenv("BB_K4_CLASSIC") != nullptr;
+    if (!pf_work.empty() && k4_classic) {
+      T.mark("deflate.profile");
       k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof, 1);
+      BB_LAUNCH_CHECK();
+    } else if (!pf_work.empty()) {
+      T.mark("deflate.gram");
+      k_gram4<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_g3, d_g4);
+      BB_LAUNCH_CHECK();
+      T.mark("deflate.profile");
+      k_profile4<<<(unsigned)pf2_work.size(), PF_THREADS, PF2_SMEM + 16, st>>>(d_lanes, d_pf2, d_g3, d_g4, d_prof, 1);
       BB_LAUNCH_CHECK();
     }
   } else if (npos_exact) {
@@ -2668,20 +3109,27 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev7, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_gram4, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_profile4, cudaFuncAttributeMaxDynamicSharedMemorySize, PF2_SMEM + 16));
   LaneDev d{};
   d.src = d_in;
   d.n = n;
-  std::vector<WorkItem> hp, pf;
+  std::vector<WorkItem> hp, pf, pf2;
   for (uint64_t s = 0; s < n; s += HP_SEG) hp.push_back(WorkItem{0, (uint32_t)s});
   for (uint64_t s = 0; s < n; s += PF_SEG) pf.push_back(WorkItem{0, (uint32_t)s});
+  for (uint64_t s = 0; s < n; s += PF2_SEG) pf2.push_back(WorkItem{0, (uint32_t)s});
   LaneDev* dl;
-  WorkItem *dh, *dp;
+  WorkItem *dh, *dp, *dp2;
+  uint32_t* dg = nullptr;
   BB_CUDA_TRY(cudaMalloc(&dl, sizeof d));
   BB_CUDA_TRY(cudaMalloc(&dh, sizeof(WorkItem) * (hp.size() + 1)));
   BB_CUDA_TRY(cudaMalloc(&dp, sizeof(WorkItem) * (pf.size() + 1)));
+  BB_CUDA_TRY(cudaMalloc(&dp2, sizeof(WorkItem) * (pf2.size() + 1)));
+  BB_CUDA_TRY(cudaMalloc(&dg, 8 * (n + 1)));
   BB_CUDA_TRY(cudaMemcpy(dl, &d, sizeof d, cudaMemcpyHostToDevice));
   if (!hp.empty()) BB_CUDA_TRY(cudaMemcpy(dh, hp.data(), sizeof(WorkItem) * hp.size(), cudaMemcpyHostToDevice));
   if (!pf.empty()) BB_CUDA_TRY(cudaMemcpy(dp, pf.data(), sizeof(WorkItem) * pf.size(), cudaMemcpyHostToDevice));
+  if (!pf2.empty()) BB_CUDA_TRY(cudaMemcpy(dp2, pf2.data(), sizeof(WorkItem) * pf2.size(), cudaMemcpyHostToDevice));
   if (n) {
     Workspace sw, w2;
     int rc = w2.reserve(4096 + 16 * (n / HP4_SEG + 2));
@@ -2692,13 +3140,23 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
     BB_CUDA_TRY(cudaStreamSynchronize(st));
   }
   if (!pf.empty() && d_prof) {
-    size_t smem = 4 * PF_WIN;
-    k_profile3<<<(unsigned)pf.size(), PF_THREADS, smem + 16, st>>>(dl, dp, d_pd, reinterpret_cast<uint2*>(d_prof), 0);
+    static const bool k4_classic = getenv("BB_K4_CLASSIC") != nullptr;
+    if (k4_classic) {
+      k_profile3<<<(unsigned)pf.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(dl, dp, d_pd,
+                                                                        reinterpret_cast<uint2*>(d_prof), 0);
+    } else {
+      k_gram4<<<(unsigned)pf.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(dl, dp, d_pd, dg, dg + n);
+      BB_LAUNCH_CHECK();
+      k_profile4<<<(unsigned)pf2.size(), PF_THREADS, PF2_SMEM + 16, st>>>(dl, dp2, dg, dg + n,
+                                                                         reinterpret_cast<uint2*>(d_prof), 0);
+    }
     BB_LAUNCH_CHECK();
   }
   BB_CUDA_TRY(cudaStreamSynchronize(st));
   cudaFree(dl);
   cudaFree(dh);
   cudaFree(dp);
+  cudaFree(dp2);
+  cudaFree(dg);
   return BB_OK;
 }
