@@ -1220,6 +1220,59 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
   }
 }
 
+// Which walk a lane takes.  K4G pays off where chains are long and same-4-gram candidates
+// sparse (bf16 exponent planes: 110 chain steps per position vs 17 to the first 4-gram
+// candidate + 11 hops); on short chains (fp16 planes: ~6 steps, no 4-gram candidates) its
+// two passes cost more than K4's one.  A sampled walk per lane (1024 positions, K3 links in
+// global memory) measures the chain length L, the steps to the first same-4-gram candidate
+// S4 and the same-4-gram hops H4; the host picks K4G where L >= 2 (S4 + H4) + 16 on average.
+constexpr uint32_t K4S_CTAS = 4;  // x 256 threads = samples per lane
+constexpr uint64_t K4G_MIN_LANE = 1u << 20;
+__global__ void __launch_bounds__(256) k_k4_sample(const LaneDev* __restrict__ lanes, const uint16_t* __restrict__ pd,
+                                                   unsigned long long* __restrict__ stat) {
+  const LaneDev L = lanes[blockIdx.y];
+  const uint64_t n = L.n;
+  if (n < K4G_MIN_LANE) return;
+  const uint32_t ns = gridDim.x * blockDim.x, k = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t p = n * (2ull * k + 1) / (2ull * ns);
+  const uint8_t* src = L.src;
+  const uint16_t* P = pd + L.pbase;
+  uint32_t len = 0, s4 = 0, h4 = 0;
+  if (p + 4 <= n) {
+    auto four = [&](uint64_t q) {
+      return (uint32_t)__ldg(src + q) | ((uint32_t)__ldg(src + q + 1) << 8) | ((uint32_t)__ldg(src + q + 2) << 16) |
+             ((uint32_t)__ldg(src + q + 3) << 24);
+    };
+    const uint32_t key = four(p);
+    const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
+    uint32_t d = P[p];
+    uint64_t c = p - d;
+    bool ok = d != 0 && d <= MAX_DIST && c != 0;
+    while (ok && len < MAX_CHAIN) {
+      len++;
+      if (four(c) == key) {
+        h4++;
+        if (!s4) s4 = len;
+      }
+      d = P[c];
+      ok = d != 0 && d < c && c - d > limit;
+      c -= d;
+    }
+    if (!s4) s4 = len;
+  }
+  const unsigned full = 0xffffffffu;
+  len = __reduce_add_sync(full, len);
+  s4 = __reduce_add_sync(full, s4);
+  h4 = __reduce_add_sync(full, h4);
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long* S = stat + 4 * blockIdx.y;
+    atomicAdd(S, (unsigned long long)len);
+    atomicAdd(S + 1, (unsigned long long)s4);
+    atomicAdd(S + 2, (unsigned long long)h4);
+    atomicAdd(S + 3, 32ull);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3S + K4S: match profiles over BUCKET-SORTED chains (variant, BB_K4_SORTED=1).
 //
@@ -2833,7 +2886,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   size_t need = 0;
   need += al(sizeof(LaneDev) * nl) + al(sizeof(ContainerDev) * nc);
   need += al(sizeof(WorkItem) * (hp_work.size() + pf_work.size() + pf2_work.size() + ad_work.size() + 4));
-  need += 2 * al(4 * pos_total);  // K4G's g3 / g4
+  need += 2 * al(4 * pos_total) + al(32ull * nl);  // K4G's g3 / g4, the walk selection
   need += al(4 * seg_lane.size()) + al(4 * blk_lane.size()) + al(4 * nl);
   need += al(2 * pos_total) + al(8 * pos_total);
   need += 2 * al(4ull * seg_total * sym_stride);            // spec + fixup symbols
@@ -2854,6 +2907,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   WorkItem* d_pf2 = W.take<WorkItem>(pf2_work.size() + 1);
   uint32_t* d_g3 = W.take<uint32_t>(pos_total);
   uint32_t* d_g4 = W.take<uint32_t>(pos_total);
+  unsigned long long* d_k4stat = W.take<unsigned long long>(4 * nl);
   WorkItem* d_ad = W.take<WorkItem>(ad_work.size() + 1);
   uint32_t* d_seg_lane = W.take<uint32_t>(seg_lane.size());
   uint32_t* d_blk_lane = W.take<uint32_t>(blk_lane.size());
@@ -2893,11 +2947,8 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
   BB_CUDA_TRY(cudaMemcpyAsync(d_cons, C.data(), sizeof(ContainerDev) * nc, cudaMemcpyHostToDevice, st));
   if (!hp_work.empty())
     BB_CUDA_TRY(cudaMemcpyAsync(d_hp, hp_work.data(), sizeof(WorkItem) * hp_work.size(), cudaMemcpyHostToDevice, st));
-  if (!pf_work.empty())
+  if (!pf_work.empty() && getenv("BB_K4_SORTED") != nullptr)
     BB_CUDA_TRY(cudaMemcpyAsync(d_pf, pf_work.data(), sizeof(WorkItem) * pf_work.size(), cudaMemcpyHostToDevice, st));
-  if (!pf2_work.empty())
-    BB_CUDA_TRY(
-        cudaMemcpyAsync(d_pf2, pf2_work.data(), sizeof(WorkItem) * pf2_work.size(), cudaMemcpyHostToDevice, st));
   if (!ad_work.empty())
     BB_CUDA_TRY(cudaMemcpyAsync(d_ad, ad_work.data(), sizeof(WorkItem) * ad_work.size(), cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_seg_lane, seg_lane.data(), 4 * seg_lane.size(), cudaMemcpyHostToDevice, st));
@@ -2915,19 +2966,55 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
       rc = hash_prev_two_phase(e->sortws, W, d_lanes, nl, lane_prefix, d_pd, st);
       if (rc) return rc;
     }
-    // K4G (default): first 3- / 4-gram candidates, then the 4-gram subsequence walk;
-    // BB_K4_CLASSIC=1: K4's full lock-step chain walk (bit-identical, 35 ms on config2)
-    static const bool k4_classic = getenv("BB_K4_CLASSIC") != nullptr;
-    if (!pf_work.empty() && k4_classic) {
-      T.mark("deflate.profile");
-      k_profile3<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof, 1);
+    // Per lane: K4's full lock-step chain walk, or K4G (first 3- / 4-gram candidates, then
+    // the 4-gram subsequence walk) where sampled chains say it is cheaper; both bit-identical.
+    // BB_K4_CLASSIC=1 / BB_K4G=1 force one walk for every lane.
+    const bool k4_classic = getenv("BB_K4_CLASSIC") != nullptr;  // read per call (tests switch them)
+    const bool k4_force_g = getenv("BB_K4G") != nullptr;
+    std::vector<char> use_g(nl, 0);
+    if (!k4_classic && !pf_work.empty()) {
+      bool any_big = false;
+      for (int i = 0; i < nl; i++) any_big = any_big || L[i].n >= K4G_MIN_LANE;
+      if (k4_force_g) {
+        std::fill(use_g.begin(), use_g.end(), 1);
+      } else if (any_big) {
+        T.mark("deflate.k4_select");
+        BB_CUDA_TRY(cudaMemsetAsync(d_k4stat, 0, 32ull * nl, st));
+        k_k4_sample<<<dim3(K4S_CTAS, nl), 256, 0, st>>>(d_lanes, d_pd, d_k4stat);
+        BB_LAUNCH_CHECK();
+        rc = pinned(e, 32ull * nl);
+        if (rc) return rc;
+        BB_CUDA_TRY(cudaMemcpyAsync(e->h_pinned, d_k4stat, 32ull * nl, cudaMemcpyDeviceToHost, st));
+        BB_CUDA_TRY(cudaStreamSynchronize(st));
+        for (int i = 0; i < nl; i++) {
+          const uint64_t* S = e->h_pinned + 4 * i;
+          use_g[i] = S[3] && S[0] >= 2 * (S[1] + S[2]) + 16 * S[3];
+        }
+      }
+    }
+    std::vector<WorkItem> w_classic, w_gram, w_prof4;
+    for (const WorkItem& w : pf_work) (use_g[w.lane] ? w_gram : w_classic).push_back(w);
+    for (const WorkItem& w : pf2_work)
+      if (use_g[w.lane]) w_prof4.push_back(w);
+    std::vector<WorkItem> both(w_classic);
+    both.insert(both.end(), w_gram.begin(), w_gram.end());
+    if (!both.empty())
+      BB_CUDA_TRY(cudaMemcpyAsync(d_pf, both.data(), sizeof(WorkItem) * both.size(), cudaMemcpyHostToDevice, st));
+    if (!w_prof4.empty())
+      BB_CUDA_TRY(
+          cudaMemcpyAsync(d_pf2, w_prof4.data(), sizeof(WorkItem) * w_prof4.size(), cudaMemcpyHostToDevice, st));
+    T.mark("deflate.profile");
+    if (!w_classic.empty()) {
+      k_profile3<<<(unsigned)w_classic.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_prof, 1);
       BB_LAUNCH_CHECK();
-    } else if (!pf_work.empty()) {
+    }
+    if (!w_gram.empty()) {
       T.mark("deflate.gram");
-      k_gram4<<<(unsigned)pf_work.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf, d_pd, d_g3, d_g4);
+      k_gram4<<<(unsigned)w_gram.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(d_lanes, d_pf + w_classic.size(), d_pd,
+                                                                           d_g3, d_g4);
       BB_LAUNCH_CHECK();
-      T.mark("deflate.profile");
-      k_profile4<<<(unsigned)pf2_work.size(), PF_THREADS, PF2_SMEM + 16, st>>>(d_lanes, d_pf2, d_g3, d_g4, d_prof, 1);
+      T.mark("deflate.profile4");
+      k_profile4<<<(unsigned)w_prof4.size(), PF_THREADS, PF2_SMEM + 16, st>>>(d_lanes, d_pf2, d_g3, d_g4, d_prof, 1);
       BB_LAUNCH_CHECK();
     }
   } else if (npos_exact) {
@@ -3140,7 +3227,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
     BB_CUDA_TRY(cudaStreamSynchronize(st));
   }
   if (!pf.empty() && d_prof) {
-    static const bool k4_classic = getenv("BB_K4_CLASSIC") != nullptr;
+    const bool k4_classic = getenv("BB_K4_CLASSIC") != nullptr;  // per call: tests check both walks
     if (k4_classic) {
       k_profile3<<<(unsigned)pf.size(), PF_THREADS, 4 * PF_WIN + 16, st>>>(dl, dp, d_pd,
                                                                         reinterpret_cast<uint2*>(d_prof), 0);

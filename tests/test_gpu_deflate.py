@@ -52,15 +52,27 @@ def _corpus():
         yield bytes(buf)
 
 
-def test_hash_prev_and_profiles_match_oracle(codec, oracle):
+@pytest.mark.parametrize("walk", ["k4g", "classic"])
+def test_hash_prev_and_profiles_match_oracle(codec, oracle, walk, monkeypatch):
+    """K3 links and K4 profiles (both walks: K4G's 4-gram subsequence, K4's full chain walk)
+    against the oracle's decomposition."""
     import torch
+    if walk == "classic":
+        monkeypatch.setenv("BB_K4_CLASSIC", "1")
+    else:
+        monkeypatch.delenv("BB_K4_CLASSIC", raising=False)
     from paper_2604_21072_b200 import _lib
     L = _lib.load()
     fn = L.bb_debug_hash_prev_profile
     fn.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(11)
     inputs = [oracle.synth_fp16(100000, 1)[1::2], oracle.synth_bf16(120000, 2)[1::2],
-              random.Random(1).randbytes(70000), b"\x07" * 40000,
-              np.random.default_rng(3).integers(0, 4, 90000, dtype=np.uint8).tobytes()]
+              oracle.synth_bf16(300000, 5)[1::2], oracle.synth_fp16(200000, 4)[0::2],
+              random.Random(1).randbytes(70000), b"\x07" * 40000, b"ab" * 30000 + b"c" * 5,
+              np.random.default_rng(3).integers(0, 4, 90000, dtype=np.uint8).tobytes(),
+              rng.integers(0, 2, 70000, dtype=np.uint8).tobytes(),
+              bytes(rng.integers(0, 3, 50, dtype=np.uint8)) * 2000,  # periodic: long matches
+              bytes(range(256)) * 300, b"xyz", b"ab"]
     for data in inputs:
         x = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
         pd = torch.zeros(len(data), dtype=torch.int16, device="cuda")
@@ -394,3 +406,16 @@ def test_sequential_inflate_on_large_streams(codec, oracle, monkeypatch):
         assert got_ok == want_ok, (trial, expected)
         if got_ok:
             assert got == want
+
+
+@pytest.mark.parametrize("walk", ["BB_K4G", "BB_K4_CLASSIC"])
+def test_forced_k4_walk_matches_zlib(codec, walk, monkeypatch):
+    """Either K4 walk forced for every lane (the default picks one per lane from sampled chain
+    statistics) gives zlib's bytes, on lanes large enough for the selection to matter."""
+    monkeypatch.setenv(walk, "1")
+    enc = codec.backend_by_id(codec.kBackendDeflate).encode
+    from paper_2604_21072_b200 import synth as S
+    cases = [S.gaussian(1 << 20, 3, True)[1::2], S.gaussian(1 << 20, 4, False)[1::2],
+             S.gaussian(600000, 5, True), np.random.default_rng(6).integers(0, 3, 1 << 20, dtype=np.uint8).tobytes()]
+    for data in cases:
+        assert enc(data) == zlib.compress(data, 6), (walk, len(data))
