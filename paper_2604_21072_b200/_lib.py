@@ -120,6 +120,13 @@ def kernel_launches() -> int:
     return int(load().bb_kernel_launches())
 
 
+def k4_positions() -> tuple:
+    """Cumulative lane positions profiled by K4's classic walk and by K4G (roofline coverage)."""
+    out = (C.c_uint64 * 2)()
+    load().bb_debug_k4_positions(out)
+    return int(out[0]), int(out[1])
+
+
 def stage_timing(enable: bool) -> None:
     load().bb_stage_timing(1 if enable else 0)
 

@@ -1227,6 +1227,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
 // global memory) measures the chain length L, the steps to the first same-4-gram candidate
 // S4 and the same-4-gram hops H4; the host picks K4G where L >= 2 (S4 + H4) + 16 on average.
 constexpr uint32_t K4S_CTAS = 4;  // x 256 threads = samples per lane
+static std::atomic<uint64_t> g_k4_positions[2];  // positions profiled by the classic walk / by K4G
 constexpr uint64_t K4G_MIN_LANE = 1u << 20;
 __global__ void __launch_bounds__(256) k_k4_sample(const LaneDev* __restrict__ lanes, const uint16_t* __restrict__ pd,
                                                    unsigned long long* __restrict__ stat) {
@@ -2992,6 +2993,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
         }
       }
     }
+    for (int i = 0; i < nl; i++) g_k4_positions[use_g[i] ? 1 : 0] += L[i].n;
     std::vector<WorkItem> w_classic, w_gram, w_prof4;
     for (const WorkItem& w : pf_work) (use_g[w.lane] ? w_gram : w_classic).push_back(w);
     for (const WorkItem& w : pf2_work)
@@ -3162,6 +3164,13 @@ extern "C" BB_API void bb_debug_pf_stats(unsigned long long* out4, int reset) {
 
 // Test hook: K3S + K4S alone on one lane (profiles without the parse's byte), for the
 // comparison with the oracle's orc_match_profile.
+// Test / bench hook: cumulative lane positions whose profiles came from the classic walk
+// (out[0]) and from K4G (out[1]) -- the coverage of each K4 kernel for the roofline accounting
+extern "C" BB_API void bb_debug_k4_positions(uint64_t* out2) {
+  out2[0] = bb::g_k4_positions[0].load();
+  out2[1] = bb::g_k4_positions[1].load();
+}
+
 extern "C" BB_API int bb_debug_profile_sorted(const uint8_t* d_in, size_t n, uint32_t* d_prof, void* stream) {
   using namespace bb;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
