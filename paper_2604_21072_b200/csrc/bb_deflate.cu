@@ -907,6 +907,69 @@ __device__ __forceinline__ void warp_range(uint64_t s, uint64_t e, uint64_t& qn,
   qe = umin64(qn + per, e);
 }
 
+// k_gram4's window word for position q: the K3 link as a distance (15 bits; 0x7fff =
+// none, outside the window, or beyond MAX_DIST -- any of them ends the walk through the
+// distance limit) | z(q) << 15 | byte q+3 << 24, where z(q) = the top three bits of
+// bytes q, q+1, q+2.  zlib's 15-bit hash ((b0 << 10) ^ (b1 << 5) ^ b2) keeps everything
+// of a 3-gram but those nine bits, and every entry of q's chain has q's hash, so along a
+// chain "same 3-gram" is "same z" and "same 4-gram" is "same z and byte 3": one load and
+// two masked compares per chain step instead of two loads and a byte permute.
+constexpr uint32_t GZ_NONE = 0x7fffu, GZ_Z = 0x00ff8000u, GZ_Z4 = 0xffff8000u;
+__device__ __forceinline__ uint32_t gz_word(uint32_t l, uint32_t i, uint32_t b) {  // b: bytes q .. q+3
+  const uint32_t d = (l && l <= i && l <= MAX_DIST) ? l : GZ_NONE;
+  const uint32_t z = ((b >> 5) & 7u) | ((b >> 10) & 0x38u) | ((b >> 15) & 0x1c0u);
+  return d | (z << 15) | (b & 0xff000000u);
+}
+__device__ __forceinline__ void gz_stage(uint32_t* w32, const uint8_t* src, const uint16_t* pdl, uint64_t n,
+                                         uint64_t wlo, uint64_t e) {
+  if (threadIdx.x == 0) w32[0] = 0;
+  const uint32_t wlen = (uint32_t)(e - wlo);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(pdl)) & 7) == 0;
+  const uint32_t nq = (wlen + 3) / 4;
+  uint32_t jf = 0;
+  if (aligned) {
+    const uint64_t lim = umin64(e >= 4 ? e - 4 : 0, n >= 8 ? n - 8 : 0);
+    jf = lim >= wlo ? (uint32_t)umin64((lim - wlo) / 4 + 1, nq) : 0;
+  }
+  constexpr int U = 4;
+  for (uint32_t j0 = threadIdx.x; j0 < jf; j0 += U * blockDim.x) {
+    uint2 l4[U];
+    uint32_t b0[U], b1[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t j = j0 + u * blockDim.x;
+      if (j < jf) {
+        const uint64_t q0 = wlo + 4 * j;
+        l4[u] = __ldg(reinterpret_cast<const uint2*>(pdl + q0));
+        b0[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0));
+        b1[u] = __ldg(reinterpret_cast<const uint32_t*>(src + q0 + 4));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t j = j0 + u * blockDim.x;
+      if (j < jf) {
+        const uint32_t i0 = 4 * j;
+        const uint32_t ls[4] = {l4[u].x & 0xffff, l4[u].x >> 16, l4[u].y & 0xffff, l4[u].y >> 16};
+        uint4 v;
+        v.x = gz_word(ls[0], i0 + 0, b0[u]);
+        v.y = gz_word(ls[1], i0 + 1, __byte_perm(b0[u], b1[u], 0x4321));
+        v.z = gz_word(ls[2], i0 + 2, __byte_perm(b0[u], b1[u], 0x5432));
+        v.w = gz_word(ls[3], i0 + 3, __byte_perm(b0[u], b1[u], 0x6543));
+        w32[i0 + 1] = v.x, w32[i0 + 2] = v.y, w32[i0 + 3] = v.z, w32[i0 + 4] = v.w;
+      }
+    }
+  }
+  for (uint32_t i = 4 * jf + threadIdx.x; i < wlen; i += blockDim.x) {
+    const uint64_t q = wlo + i;
+    uint32_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      if (q + k < n) b |= (uint32_t)__ldg(src + q + k) << (8 * k);
+    w32[i + 1] = gz_word(pdl[q], i, b);
+  }
+}
+
 __global__ void __launch_bounds__(PF_THREADS, 1) k_gram4(const LaneDev* __restrict__ lanes,
                                                          const WorkItem* __restrict__ work,
                                                          const uint16_t* __restrict__ pd, uint32_t* __restrict__ g3,
@@ -918,46 +981,50 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_gram4(const LaneDev* __restri
   const uint64_t s = w.start;
   const uint64_t e = umin64(s + PF_SEG, n);
   const uint64_t wlo = s > WSIZE ? s - WSIZE : 0;
-  const uint32_t wlen = (uint32_t)(e - wlo) + 16;
-  pf_stage_links(w32, L.src, pd + L.pbase, n, wlo, e, wlen);
+  gz_stage(w32, L.src, pd + L.pbase, n, wlo, e);
   __syncthreads();
-  uint32_t* G3 = g3 + L.pbase;
-  uint32_t* G4 = g4 + L.pbase;
+  // positions as 1-based window indices (32-bit): ix = p - wlo + 1
+  uint32_t* G3 = g3 + L.pbase + wlo - 1;
+  uint32_t* G4 = g4 + L.pbase + wlo - 1;
+  const uint32_t nrel = (uint32_t)umin64(n - wlo, 1u << 30);  // n as a window index bound
+  const uint32_t ix0 = wlo == 0 ? 1u : 0u;                     // absolute position 0 (NIL), if in the window
   const unsigned lt = (1u << (threadIdx.x & 31)) - 1;
-  uint64_t qn, qe;
-  warp_range(s, e, qn, qe);
-  const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w32);
-  uint64_t p = 0;
-  bool has = false, done = true, found4 = false, four = false;
+  uint32_t qn, qe;
+  {
+    uint64_t a, b;
+    warp_range(s, e, a, b);
+    qn = (uint32_t)(a - wlo) + 1, qe = (uint32_t)(b - wlo) + 1;
+  }
+  const int sw = (int)__cvta_generic_to_shared(w32);
+  bool has = false, done = true, four = false;
   // lane state: cb = shared byte address of the current candidate's word; a lane without a
   // walk sits on the sentinel word 0 with done set
-  uint32_t ix = 0, key = 0, cb = sw, stp = 0, limb = sw, f3c = 0, f3s = 0, hd = 0;
+  uint32_t ix = 0, key = 0, stp = 0, f3s = 0, hd = 0;
+  int cb = sw, limb = sw, f3c = 0;
   for (;;) {
     // refill (once per batch): idle lanes take the warp's next positions in order
     const unsigned need = __ballot_sync(0xffffffffu, !has);
     if (need && qn < qe) {
-      const uint64_t myp = qn + __popc(need & lt);
-      qn = umin64(qn + __popc(need), qe);
+      const uint32_t myp = qn + __popc(need & lt);
+      qn = min(qn + __popc(need), qe);
       if (!has && myp < qe) {
-        p = myp;
-        ix = (uint32_t)(p - wlo) + 1;
+        ix = myp;
         const uint32_t wp = w32[ix];
-        const uint32_t c0 = wp & 0xffff, d0 = ix - c0;
-        if (p + MIN_MATCH <= n && c0 != 0 && d0 <= MAX_DIST && wlo + c0 - 1 != 0) {
-          const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
-          limb = sw + 4 * (limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0u);
+        const uint32_t d0 = wp & GZ_NONE;
+        // zlib: the head must be within MAX_DIST and not absolute position 0 (NIL)
+        if (ix + 2 <= nrel && d0 != GZ_NONE && ix - d0 != ix0) {
+          limb = sw + 4 * max((int)ix - (int)MAX_DIST, 1);
           hd = G3_LIVE | (d0 == MAX_DIST ? G3_FLAG : 0u);
-          four = p + 4 <= n;
-          key = __byte_perm(wp, w32[ix + 2], 0x7632);  // bytes p .. p + 3
-          cb = sw + 4 * c0;
+          four = ix + 3 <= nrel;
+          key = wp & GZ_Z4;
+          cb = sw + 4 * (int)(ix - d0);
           stp = 1;
-          f3c = f3s = 0;
-          found4 = false;
+          f3s = 0;
           has = true;
           done = false;
         } else {
-          G3[p] = 0;
-          G4[p] = 0;
+          G3[ix] = 0;
+          G4[ix] = 0;
         }
       }
     }
@@ -968,17 +1035,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_gram4(const LaneDev* __restri
     // GB chain steps, branch-free; a lane whose walk ended stays on its last candidate
 #pragma unroll
     for (int t = 0; t < GB_STEPS; t++) {
-      uint32_t wc, wc2;
+      uint32_t wc;
       asm("ld.shared.u32 %0, [%1];" : "=r"(wc) : "r"(cb));
-      asm("ld.shared.u32 %0, [%1+8];" : "=r"(wc2) : "r"(cb));
-      const uint32_t m = __byte_perm(wc, wc2, 0x7632) ^ key;  // candidate bytes 0..3 vs the position's
-      const bool h3 = !done && (m & 0xffffffu) == 0;
+      const uint32_t x = wc ^ key;
+      const bool h3 = !done && (x & GZ_Z) == 0;
       const bool first3 = h3 && f3s == 0;
       f3c = first3 ? cb : f3c;
       f3s = first3 ? stp : f3s;
-      const bool h4 = h3 && four && m == 0;
-      found4 = found4 || h4;
-      const uint32_t nb = sw + ((wc & 0xffffu) << 2);  // entries after the head must lie above the limit
+      const bool h4 = h3 && (x & GZ_Z4) == 0;
+      const int nb = cb - 4 * (int)(wc & GZ_NONE);  // entries after the head must lie above the limit
       const bool end = h4 || stp >= MAX_CHAIN || nb <= limb;
       const bool adv = !done && !end;
       done = done || end;
@@ -986,8 +1051,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_gram4(const LaneDev* __restri
       stp = adv ? stp + 1 : stp;
     }
     if (has && done) {
-      G3[p] = f3s ? (ix - ((f3c - sw) >> 2)) | (f3s << 15) | hd : hd;
-      G4[p] = found4 ? (ix - ((cb - sw) >> 2)) | (stp << 15) : 0u;
+      // the walk ended on a same-4-gram candidate iff the candidate it stopped on is one
+      const uint32_t c4 = (uint32_t)(cb - sw) >> 2;
+      const bool found4 = four && ((w32[c4] ^ key) & GZ_Z4) == 0;
+      G3[ix] = f3s ? (ix - ((uint32_t)(f3c - sw) >> 2)) | (f3s << 15) | hd : hd;
+      G4[ix] = found4 ? (ix - c4) | (stp << 15) : 0u;
       has = false;
     }
   }
