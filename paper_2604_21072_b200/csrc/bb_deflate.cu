@@ -1151,11 +1151,18 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
   const uint32_t skb = sw + 4 * PF2_WIN;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
-  uint64_t qn, qe;
-  warp_range(s, e, qn, qe);
+  // positions as 1-based window indices (32-bit): ip1 = p - wlo + 1
+  const uint32_t* G3w = G3 + wlo - 1;
+  uint2* profw = prof + L.pbase + wlo - 1;
+  const uint32_t nrel = (uint32_t)umin64(n - wlo, 1u << 30);
+  uint32_t qn, qe;
+  {
+    uint64_t a, b;
+    warp_range(s, e, a, b);
+    qn = (uint32_t)(a - wlo) + 1, qe = (uint32_t)(b - wlo) + 1;
+  }
   // the warp's next 32 positions' g3 records, one per lane, loaded a batch ahead
-  uint32_t gbuf = qn + lane < qe ? __ldg(G3 + qn + lane) : 0u;
-  uint64_t p = 0;
+  uint32_t gbuf = qn + lane < qe ? __ldg(G3w + qn + lane) : 0u;
   bool has = false, done = true, snap = false;
   uint32_t ip1 = 0, maxl = 0, nice = 0, lim1 = 0, flag = 0, best = MIN_MATCH - 1, bestd = 0, r32 = 0;
   uint32_t key = 0;  // bytes (best - 1, best) of p (best >= 4 while a lane walks)
@@ -1163,7 +1170,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
   auto store = [&](bool live) {
     const uint32_t yb = with_bytes ? (w32[ip1 - 1] << 8) & 0xff000000u : (live ? flag : 0u);
     if (live && !snap) r32 = prof_pack(best, bestd);
-    prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
+    profw[ip1] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
   };
   // match length of candidate cx whose first `from` (>= 4) bytes are known to match p's
   auto extend = [&](uint32_t cx, uint32_t from) {
@@ -1183,23 +1190,21 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
     if (need && qn < qe) {
       const uint32_t cnt = __popc(need), r = __popc(need & lt);
       const uint32_t gg = __shfl_sync(0xffffffffu, gbuf, r & 31);
-      const uint64_t myp = qn + r;
+      const uint32_t myp = qn + r;
       // the buffer moves on by cnt positions; the lanes past its end load new records
       const uint32_t moved = __shfl_down_sync(0xffffffffu, gbuf, cnt & 31);
-      const uint64_t qn2 = umin64(qn + cnt, qe);
-      gbuf = lane + cnt < 32 ? moved : (qn2 + lane < qe ? __ldg(G3 + qn2 + lane) : 0u);
+      const uint32_t qn2 = min(qn + cnt, qe);
+      gbuf = lane + cnt < 32 ? moved : (qn2 + lane < qe ? __ldg(G3w + qn2 + lane) : 0u);
       if (!has && myp < qe) {
-        p = myp;
-        ip1 = (uint32_t)(p - wlo) + 1;
+        ip1 = myp;
         const uint32_t d3 = gg & 0x7fff;
         flag = gg & G3_FLAG ? PROF_AT_MAXDIST : 0u;
         best = MIN_MATCH - 1, bestd = 0, r32 = 0, snap = false;
         bool walk = false;
         if (d3) {  // live, with a same-3-gram candidate within the budget
-          const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
+          const uint32_t la = min(nrel - ip1 + 1, 1u << 20);
           nice = min(NICE_LENGTH, la), maxl = min(MAX_MATCH, la);
-          const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
-          lim1 = limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0;
+          lim1 = (uint32_t)max((int)ip1 - (int)MAX_DIST, 1);
           // the first same-3-gram candidate (the only source of a match of exactly 3)
           const uint32_t c3 = ip1 - d3, s3 = (gg >> 15) & 0xff;
           if (s3 > 32) snap = true;  // r32 stays "no match"
