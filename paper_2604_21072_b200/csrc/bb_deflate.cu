@@ -1172,6 +1172,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
     if (live && !snap) r32 = prof_pack(best, bestd);
     profw[ip1] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
   };
+  // a walking lane has best >= 4 (its first same-4-gram candidate matched), so neither
+  // of prof_pack's "no match" rules can apply
+  auto store_walked = [&]() {
+    const uint32_t pk = best | (bestd << 9);
+    const uint32_t yb = with_bytes ? (w32[ip1 - 1] << 8) & 0xff000000u : flag;
+    profw[ip1] = make_uint2(pk | flag, (snap ? r32 : pk) | yb);
+  };
   // match length of candidate cx whose first `from` (>= 4) bytes are known to match p's
   auto extend = [&](uint32_t cx, uint32_t from) {
     uint32_t len = from;
@@ -1269,7 +1276,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
       mask &= mask - 1;
       const uint32_t cx = pf_pick(cand, t), sc = pf_pick(cst, t);
       if (sc > 32 && !snap) {  // the budget-32 result: everything before this candidate
-        r32 = prof_pack(best, bestd);
+        r32 = best | (bestd << 9);  // best >= 4 while walking
         snap = true;
       }
       // re-test against the current best if it grew in this flush
@@ -1287,7 +1294,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
     }
     if (improved) key = w32[ip1 + best - 1] >> 16;
     if (has && done) {
-      store(true);
+      store_walked();
       has = false;
     }
   }
