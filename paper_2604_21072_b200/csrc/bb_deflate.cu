@@ -1251,8 +1251,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
     }
     // PB_STEPS hops along the 4-gram subsequence, branch-free; candidates passing the quick
     // test (bytes best - 1, best of the lagging best) are recorded
-    uint32_t cand[PB_STEPS], cst[PB_STEPS];
-    uint32_t mask = 0;
+    uint32_t cand[PB_STEPS];
+    uint32_t mask = 0, m32 = 0;  // m32: the steps whose candidate lies beyond the budget-32 prefix
     const uint32_t qb = sw + 4 * best - 2;  // + 4 c: the candidate's bytes (best - 1, best)
 #pragma unroll
     for (int t = 0; t < PB_STEPS; t++) {
@@ -1261,7 +1261,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
       asm("ld.shared.u16 %0, [%1];" : "=r"(we) : "r"(qb + 4 * c));
       asm("ld.shared.u8 %0, [%1];" : "=r"(k) : "r"(skb + c));
       cand[t] = c;
-      cst[t] = stp;
+      m32 |= stp > 32 ? 1u << t : 0u;
       mask |= (!done && we == key) ? 1u << t : 0u;
       const uint32_t nc = wc & 0xffff, ns = stp + k;
       const bool adv = !done && nc > lim1 && ns <= MAX_CHAIN;
@@ -1274,14 +1274,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
     while (mask) {
       const int t = __ffs(mask) - 1;
       mask &= mask - 1;
-      const uint32_t cx = pf_pick(cand, t), sc = pf_pick(cst, t);
-      if (sc > 32 && !snap) {  // the budget-32 result: everything before this candidate
+      const uint32_t cx = pf_pick(cand, t);
+      if (((m32 >> t) & 1) && !snap) {  // the budget-32 result: everything before this candidate
         r32 = best | (bestd << 9);  // best >= 4 while walking
         snap = true;
       }
       // re-test against the current best if it grew in this flush
       if (improved && (w32[cx + best - 1] >> 16) != (w32[ip1 + best - 1] >> 16)) continue;
-      const uint32_t len = extend(cx, 4);
+      // bytes 0-3 (same 4-gram) and best - 1, best (quick test) are known to match: up to
+      // best = 5 that is every byte before best + 1
+      const uint32_t len = extend(cx, best <= 5 ? best + 1 : 4);
       if (len > best) {
         best = len;
         bestd = ip1 - cx;
