@@ -1967,7 +1967,7 @@ struct TreesState {
   TreeArr<L_CODES> lt;
   TreeArr<D_CODES> dt;
   TreeArr<BL_CODES> blt;
-  alignas(16) uint32_t heap[HEAP_SIZE + 1];
+  alignas(16) uint32_t heap[HEAP_SIZE + 7];  // + grandson-load padding (t_down)
   uint16_t bl_count[16];
   uint64_t opt_len, static_len;
   int lmax, dmax, blmax;
@@ -1983,13 +1983,43 @@ __device__ __forceinline__ uint32_t t_node(uint32_t e) { return e & 0x3ff; }
 __device__ __forceinline__ uint32_t t_freq(uint32_t e) { return e >> 15; }
 __device__ __forceinline__ uint32_t t_depth(uint32_t e) { return (e >> 10) & 0x1f; }
 
-// trees.c pqdownheap with smaller(n, m) == key(n) <= key(m)
-__device__ __forceinline__ void t_down(uint32_t* heap, int heap_len, int k) {
+// trees.c pqdownheap with smaller(n, m) == key(n) <= key(m).  The walk down is one
+// dependent shared-memory load per level; here the four grandsons (heap[4k .. 4k + 3],
+// one 16-byte load) are fetched while the sons are compared, so each level's load was
+// issued a level earlier.  (heap is padded: a grandson load may read past heap_len.)
+// Used where few blocks run (K6 latency-bound: config1's 0.39 -> 0.30 ms); with many blocks
+// per SM the extra loads cost shared-memory issue slots (config2 3.16 -> 3.28 ms), so the
+// plain walk below serves that case.
+__device__ __forceinline__ void t_down_pf(uint32_t* heap, int heap_len, int k) {
+  const uint32_t v = heap[k];
+  const uint32_t vk = v >> 10;
+  int j = k << 1;
+  if (j <= heap_len) {
+    uint2 sons = *reinterpret_cast<const uint2*>(heap + j);  // j even: 8-byte aligned
+    uint4 gs = *reinterpret_cast<const uint4*>(heap + 2 * j);  // 2j = 4k: 16-byte aligned
+    for (;;) {
+      uint32_t hj = sons.x;
+      bool right = false;
+      if (j < heap_len && (sons.y >> 10) <= (hj >> 10)) {
+        right = true;
+        hj = sons.y;
+      }
+      if (vk <= (hj >> 10)) break;
+      heap[k] = hj;
+      k = j + right;
+      j = k << 1;
+      if (j > heap_len) break;
+      sons = right ? make_uint2(gs.z, gs.w) : make_uint2(gs.x, gs.y);
+      gs = *reinterpret_cast<const uint4*>(heap + 2 * j);
+    }
+  }
+  heap[k] = v;
+}
+__device__ __forceinline__ void t_down_plain(uint32_t* heap, int heap_len, int k) {
   const uint32_t v = heap[k];
   const uint32_t vk = v >> 10;
   int j = k << 1;
   while (j <= heap_len) {
-    // j is even: both sons in one 64-bit shared load (heap is 16-byte aligned)
     const uint2 sons = *reinterpret_cast<const uint2*>(heap + j);
     uint32_t hj = sons.x;
     if (j < heap_len) {
@@ -2006,10 +2036,15 @@ __device__ __forceinline__ void t_down(uint32_t* heap, int heap_len, int k) {
   }
   heap[k] = v;
 }
+template <bool LAT>
+__device__ __forceinline__ void t_down(uint32_t* heap, int heap_len, int k) {
+  if (LAT) t_down_pf(heap, heap_len, k);
+  else t_down_plain(heap, heap_len, k);
+}
 
 // trees.c build_tree + gen_bitlen + gen_codes (single thread)
 // KIND: 0 lit/len, 1 dist, 2 bit-length
-template <int KIND, int ELEMS>
+template <int KIND, bool LAT, int ELEMS>
 __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
   constexpr int max_length = KIND == 2 ? 7 : 15;
   constexpr int base = KIND == 0 ? 257 : 0;
@@ -2032,12 +2067,12 @@ __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
     if (KIND == 0) s->static_len -= c_z.sl_len[node];
     else if (KIND == 1) s->static_len -= 5;
   }
-  for (n = heap_len / 2; n >= 1; n--) t_down(heap, heap_len, n);
+  for (n = heap_len / 2; n >= 1; n--) t_down<LAT>(heap, heap_len, n);
   node = ELEMS;
   do {
     const uint32_t en = heap[1];
     heap[1] = heap[heap_len--];
-    t_down(heap, heap_len, 1);
+    t_down<LAT>(heap, heap_len, 1);
     const uint32_t em = heap[1];
     heap[--heap_max] = en;
     heap[--heap_max] = em;
@@ -2046,27 +2081,62 @@ __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
     t->dad[t_node(en)] = t->dad[t_node(em)] = (uint16_t)node;
     heap[1] = t_entry(f & 0xffff, d, node);  // ush Freq, as in zlib
     node++;
-    t_down(heap, heap_len, 1);
+    t_down<LAT>(heap, heap_len, 1);
   } while (heap_len >= 2);
   heap[--heap_max] = heap[1];
 
-  // gen_bitlen
   int h, bits, overflow = 0;
-  for (bits = 0; bits <= 15; bits++) s->bl_count[bits] = 0;
-  t->len[t_node(heap[heap_max])] = 0;
-  for (h = heap_max + 1; h < (int)HEAP_SIZE; h++) {
-    n = t_node(heap[h]);
-    bits = t->len[t->dad[n]] + 1;
-    if (bits > max_length) bits = max_length, overflow++;
-    t->len[n] = (uint8_t)bits;
-    if (n > max_code) continue;
-    s->bl_count[bits]++;
-    int xbits = 0;
-    if (n >= base) xbits = KIND == 0 ? c_extra_lbits[n - base] : KIND == 1 ? c_extra_dbits[n - base] : c_extra_blbits[n - base];
-    uint32_t f = t->freq[n];
-    s->opt_len += (uint64_t)f * (uint32_t)(bits + xbits);
-    if (KIND == 0) s->static_len += (uint64_t)f * (uint32_t)(c_z.sl_len[n] + xbits);
-    else if (KIND == 1) s->static_len += (uint64_t)f * (uint32_t)(5 + xbits);
+  if (LAT) {
+    // gen_bitlen (latency variant, few blocks).  The walk is serial through len[dad[n]]; the next entry's node and dad
+    // are loaded an iteration ahead, and the sums and the length counts (16-bit fields of
+    // four registers) stay in registers instead of read-modify-writes of shared memory.
+    t->len[t_node(heap[heap_max])] = 0;
+    uint64_t opt = s->opt_len, stat = s->static_len, blc[4] = {0, 0, 0, 0};
+    h = heap_max + 1;
+    uint32_t nn = h < (int)HEAP_SIZE ? t_node(heap[h]) : 0u;
+    uint32_t dd = t->dad[nn];
+    for (; h < (int)HEAP_SIZE; h++) {
+      n = (int)nn;
+      const uint32_t dad = dd;
+      if (h + 1 < (int)HEAP_SIZE) {
+        nn = t_node(heap[h + 1]);
+        dd = t->dad[nn];
+      }
+      bits = t->len[dad] + 1;
+      if (bits > max_length) bits = max_length, overflow++;
+      t->len[n] = (uint8_t)bits;
+      if (n > max_code) continue;
+      const int q = bits >> 2;
+      const uint64_t inc = 1ull << (16 * (bits & 3));
+#pragma unroll
+      for (int r = 0; r < 4; r++) blc[r] += q == r ? inc : 0ull;
+      int xbits = 0;
+      if (n >= base) xbits = KIND == 0 ? c_extra_lbits[n - base] : KIND == 1 ? c_extra_dbits[n - base] : c_extra_blbits[n - base];
+      uint32_t f = t->freq[n];
+      opt += (uint64_t)f * (uint32_t)(bits + xbits);
+      if (KIND == 0) stat += (uint64_t)f * (uint32_t)(c_z.sl_len[n] + xbits);
+      else if (KIND == 1) stat += (uint64_t)f * (uint32_t)(5 + xbits);
+    }
+    s->opt_len = opt;
+    s->static_len = stat;
+    for (bits = 0; bits <= 15; bits++) s->bl_count[bits] = (uint16_t)(blc[bits >> 2] >> (16 * (bits & 3)));
+  } else {
+    for (bits = 0; bits <= 15; bits++) s->bl_count[bits] = 0;
+    t->len[t_node(heap[heap_max])] = 0;
+    for (h = heap_max + 1; h < (int)HEAP_SIZE; h++) {
+      n = t_node(heap[h]);
+      bits = t->len[t->dad[n]] + 1;
+      if (bits > max_length) bits = max_length, overflow++;
+      t->len[n] = (uint8_t)bits;
+      if (n > max_code) continue;
+      s->bl_count[bits]++;
+      int xbits = 0;
+      if (n >= base) xbits = KIND == 0 ? c_extra_lbits[n - base] : KIND == 1 ? c_extra_dbits[n - base] : c_extra_blbits[n - base];
+      uint32_t f = t->freq[n];
+      s->opt_len += (uint64_t)f * (uint32_t)(bits + xbits);
+      if (KIND == 0) s->static_len += (uint64_t)f * (uint32_t)(c_z.sl_len[n] + xbits);
+      else if (KIND == 1) s->static_len += (uint64_t)f * (uint32_t)(5 + xbits);
+    }
   }
   if (overflow) {
     do {
@@ -2281,11 +2351,11 @@ __global__ void __launch_bounds__(NT) k_blocks(const LaneDev* __restrict__ lanes
   if (threadIdx.x == 0) {
     S.opt_len = 0;
     S.static_len = 0;
-    S.lmax = t_build_tree<0>(&S, &S.lt);
-    S.dmax = t_build_tree<1>(&S, &S.dt);
+    S.lmax = t_build_tree<0, (NT > 32)>(&S, &S.lt);
+    S.dmax = t_build_tree<1, (NT > 32)>(&S, &S.dt);
     t_scan_tree(&S, &S.lt, S.lmax);
     t_scan_tree(&S, &S.dt, S.dmax);
-    t_build_tree<2>(&S, &S.blt);
+    t_build_tree<2, (NT > 32)>(&S, &S.blt);
     int max_blindex;
     for (max_blindex = BL_CODES - 1; max_blindex >= 3; max_blindex--)
       if (S.blt.len[c_bl_order[max_blindex]] != 0) break;
