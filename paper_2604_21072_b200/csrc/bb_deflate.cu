@@ -422,6 +422,153 @@ __global__ void __launch_bounds__(32 * HP7_W) k_hash_prev7(const LaneDev* __rest
   for (int i = threadIdx.x; i < 32768 * 2 / 16; i += blockDim.x) dst[i] = h4[i];
 }
 
+// K3 (current): k_hash_prev7's warps and tile order, with each 128-position tile's
+// same-hash structure found before the in-order phase instead of inside it.  A warp sorts
+// its tile's (hash, index) keys (bitonic, four per lane); in sorted order a position's
+// previous occurrence inside the tile is its left neighbour, the first occurrence of a hash
+// reads the head table, the last one writes it.  The in-order phase is then only those
+// loads and stores -- no data flows from the loads to the stores, so a tile's turn costs
+// their issue, not k_hash_prev7's four load -> store -> __syncwarp rounds.
+__device__ __forceinline__ void hp_sort128(uint32_t (&v)[4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 128; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const int rp = r ^ (j >> 5);
+          if (rp > r) {
+            const bool up = ((32 * r + lane) & k) == 0;
+            const uint32_t a = v[r], b = v[rp];
+            v[r] = up ? min(a, b) : max(a, b);
+            v[rp] = up ? max(a, b) : min(a, b);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool up = ((32 * r + lane) & k) == 0;
+          const bool lo = ((lane & j) == 0) == up;
+          v[r] = lo ? min(v[r], o) : max(v[r], o);
+        }
+      }
+    }
+  }
+}
+
+#ifndef HP8_W_OVR
+#define HP8_W_OVR 8  // sweep (config2 K3+fix ms): 8 4.39, 10 4.47, 12 4.37, 15 4.58; 15 with 2 tiles per turn 5.31
+#endif
+#ifndef HP8_TP
+#define HP8_TP 1
+#endif
+constexpr int HP8_W = HP8_W_OVR;
+static_assert(HP8_W <= 15, "named barriers 1 .. 15");
+__global__ void __launch_bounds__(32 * HP8_W) k_hash_prev8(const LaneDev* __restrict__ lanes,
+                                                          const WorkItem* __restrict__ work,
+                                                          uint16_t* __restrict__ pd,
+                                                          uint16_t* __restrict__ seg_heads) {
+  constexpr int TP = HP8_TP;
+  extern __shared__ uint16_t hp8_head[];  // position - s + 1 (0 = none)
+  const WorkItem w = work[blockIdx.x];
+  const LaneDev L = lanes[w.lane];
+  const uint64_t n = L.n;
+  const uint64_t s = w.start;
+  const uint64_t e = umin64(s + HP4_SEG, n);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint16_t* head = hp8_head;
+  uint4* h4 = reinterpret_cast<uint4*>(head);
+  const uint8_t* src = L.src;
+  uint16_t* out = pd + L.pbase + s;
+  const uint32_t se = (uint32_t)(e - s);  // segment positions
+  const uint32_t sv = (uint32_t)umin64(n - s, 1u << 30) >= 2 ? (uint32_t)umin64(n - s, 1u << 30) - 2 : 0;  // q - s < sv: 3 bytes of lookahead
+  for (int i = threadIdx.x; i < 32768 * 2 / 16; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+  const uint32_t ntiles = (se + 127) / 128;
+  uint32_t cw[TP], cx[TP];
+#pragma unroll
+  for (int u = 0; u < TP; u++) {
+    cw[u] = cx[u] = 0;
+    const uint32_t t = (uint32_t)wid * TP + u;
+    if (t < ntiles) hp_load_tile(src, n, s + 128ull * t, lane, cw[u], cx[u]);
+  }
+  __syncthreads();
+  for (uint32_t t0 = (uint32_t)wid * TP; t0 < ntiles; t0 += HP8_W * TP) {
+    uint32_t nw[TP], nx[TP];
+#pragma unroll
+    for (int u = 0; u < TP; u++) {  // this warp's next turn
+      nw[u] = nx[u] = 0;
+      const uint32_t t = t0 + HP8_W * TP + u;
+      if (t < ntiles) hp_load_tile(src, n, s + 128ull * t, lane, nw[u], nx[u]);
+    }
+    // per tile and sorted slot r: key = hash (16 bits; invalid positions get 0x8000 + index,
+    // unique) << 7 | tile index; first / last occurrence flags; in-tile distance
+    uint32_t key[TP][4], d[TP][4];
+    unsigned fl[TP];  // bit r: first occurrence (reads the head), bit 4 + r: last (writes it)
+#pragma unroll
+    for (int u = 0; u < TP; u++) {
+      const uint32_t c = 128u * (t0 + u);  // segment-relative tile start
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const uint32_t i = 32u * r + lane, q = c + i;
+        const bool valid = q < se && q < sv;
+        const uint32_t hh = hp_hash_at(cw[u], cx[u], r, lane);
+        key[u][r] = ((valid ? hh : 0x8000u + i) << 7) | i;
+      }
+      hp_sort128(key[u]);
+      fl[u] = 0;
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const uint32_t k = key[u][r];
+        uint32_t left = __shfl_up_sync(0xffffffffu, k, 1);
+        uint32_t right = __shfl_down_sync(0xffffffffu, k, 1);
+        const uint32_t lprev = __shfl_sync(0xffffffffu, r > 0 ? key[u][r > 0 ? r - 1 : 0] : 0u, 31);
+        const uint32_t rnext = __shfl_sync(0xffffffffu, r < 3 ? key[u][r < 3 ? r + 1 : 3] : 0u, 0);
+        if (lane == 0) left = r > 0 ? lprev : 0xffffffffu;
+        if (lane == 31) right = r < 3 ? rnext : 0xffffffffu;
+        const bool real = (k >> 22) == 0;  // hash < 0x8000
+        const bool first = real && (left >> 7) != (k >> 7);
+        const bool last = real && (right >> 7) != (k >> 7);
+        fl[u] |= (first ? 1u << r : 0u) | (last ? 16u << r : 0u);
+        d[u][r] = real ? (first ? 0u : (k & 127) - (left & 127)) : 0u;
+      }
+    }
+    // wait for the previous turn's head updates (named barrier: its warp arrives, this one syncs;
+    // ids 1 .. HP8_W, so HP8_W <= 15)
+    if (t0 > 0) asm volatile("bar.sync %0, 64;" ::"r"(1 + (wid + HP8_W - 1) % HP8_W) : "memory");
+    uint32_t hv[TP][4];
+#pragma unroll
+    for (int u = 0; u < TP; u++) {
+      const uint32_t c = 128u * (t0 + u);
+#pragma unroll
+      for (int r = 0; r < 4; r++) hv[u][r] = (fl[u] >> r) & 1 ? head[key[u][r] >> 7] : 0u;
+      __syncwarp();  // the tile's loads see the table before its own stores
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+        if ((fl[u] >> (4 + r)) & 1) head[key[u][r] >> 7] = (uint16_t)(c + (key[u][r] & 127) + 1);
+      __syncwarp();
+    }
+    if (t0 + TP < ntiles) asm volatile("bar.arrive %0, 64;" ::"r"(1 + wid) : "memory");
+#pragma unroll
+    for (int u = 0; u < TP; u++) {
+      const uint32_t c = 128u * (t0 + u);
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const uint32_t q = c + (key[u][r] & 127);
+        uint32_t dd = d[u][r];
+        if ((fl[u] >> r) & 1) dd = hv[u][r] ? q + 1 - hv[u][r] : 0xffffu;  // 0xffff: the previous segment
+        if (q < se) out[q] = (uint16_t)dd;
+      }
+      cw[u] = nw[u], cx[u] = nx[u];
+    }
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(seg_heads + (uint64_t)blockIdx.x * 32768);
+  for (int i = threadIdx.x; i < 32768 * 2 / 16; i += blockDim.x) dst[i] = h4[i];
+}
+
 // k_hash_fix2: one CTA per segment, eight positions per thread and step
 // (one 16-byte load of their links); only positions marked 0xffff compute their
 // hash and read the previous segment's final head table.
@@ -495,10 +642,13 @@ static int hash_prev_two_phase(Workspace& sortws, Workspace& W, const LaneDev* d
   BB_CUDA_TRY(cudaMemcpyAsync(d_seg0, seg0.data(), 4 * nl, cudaMemcpyHostToDevice, st));
   BB_CUDA_TRY(cudaMemcpyAsync(d_lp, lane_prefix.data(), 8 * (nl + 1), cudaMemcpyHostToDevice, st));
   static const bool k3_single = getenv("BB_K3_SINGLE_WARP") != nullptr;
+  static const bool k3_v7 = getenv("BB_K3_V7") != nullptr;
   if (k3_single)
     k_hash_prev6<<<(unsigned)work.size(), 32, 65536, st>>>(d_lanes, d_work, d_pd, heads);
-  else
+  else if (k3_v7)
     k_hash_prev7<<<(unsigned)work.size(), 32 * HP7_W, 65536, st>>>(d_lanes, d_work, d_pd, heads);
+  else
+    k_hash_prev8<<<(unsigned)work.size(), 32 * HP8_W, 65536, st>>>(d_lanes, d_work, d_pd, heads);
   BB_LAUNCH_CHECK();
   k_hash_fix2<<<(unsigned)work.size(), 256, 0, st>>>(d_lanes, d_work, d_pd, heads);
   BB_LAUNCH_CHECK();
@@ -2965,6 +3115,7 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
     BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev7, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev8, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_gram4, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
     BB_CUDA_TRY(cudaFuncSetAttribute(k_profile4, cudaFuncAttributeMaxDynamicSharedMemorySize, PF2_SMEM + 16));
@@ -3356,6 +3507,7 @@ extern "C" BB_API int bb_debug_hash_prev_profile(const uint8_t* d_in, size_t n, 
   BB_CUDA_TRY(cudaMemcpyToSymbol(c_z, &t, sizeof t));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev6, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev7, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  BB_CUDA_TRY(cudaFuncSetAttribute(k_hash_prev8, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_profile3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_gram4, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PF_WIN + 16));
   BB_CUDA_TRY(cudaFuncSetAttribute(k_profile4, cudaFuncAttributeMaxDynamicSharedMemorySize, PF2_SMEM + 16));
