@@ -1399,6 +1399,53 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
       if (qn >= qe) break;
       continue;
     }
+#ifndef PF4_NO_PAUSE
+    // PB_STEPS hops along the 4-gram subsequence, branch-free.  A lane whose candidate passes
+    // the quick test (bytes best - 1, best) pauses there for the rest of the batch; after the
+    // batch every paused lane extends its one candidate.  best never lags the test, and the
+    // extension is one candidate per lane instead of each lane's recorded list in turn (the
+    // warp ran the longest list: ~45 % of the kernel's instructions).
+    const uint32_t qb = sw + 4 * best - 2;  // + 4 c: the candidate's bytes (best - 1, best)
+    bool paused = false;
+    uint32_t pc = 0, ps = 0;  // the paused-on candidate and its chain step
+#pragma unroll
+    for (int t = 0; t < PB_STEPS; t++) {
+      uint32_t wc, we, k;
+      asm("ld.shared.u32 %0, [%1];" : "=r"(wc) : "r"(sw + 4 * c));
+      asm("ld.shared.u16 %0, [%1];" : "=r"(we) : "r"(qb + 4 * c));
+      asm("ld.shared.u8 %0, [%1];" : "=r"(k) : "r"(skb + c));
+      const bool live = !done && !paused;
+      const bool hit = live && we == key;
+      pc = hit ? c : pc;
+      ps = hit ? stp : ps;
+      const uint32_t nc = wc & 0xffff, ns = stp + k;
+      const bool ok = nc > lim1 && ns <= MAX_CHAIN;
+      const bool adv = live && ok;
+      done = done || (live && !ok);
+      paused = paused || hit;
+      c = adv ? nc : c;
+      stp = adv ? ns : stp;
+    }
+    if (__any_sync(0xffffffffu, paused) && paused) {
+      if (ps > 32 && !snap) {  // the budget-32 result: everything before this candidate
+        r32 = best | (bestd << 9);  // best >= 4 while walking
+        snap = true;
+      }
+      // bytes 0-3 (same 4-gram) and best - 1, best (quick test) are known to match: up to
+      // best = 5 that is every byte before best + 1
+      const uint32_t len = extend(pc, best <= 5 ? best + 1 : 4);
+      if (len > best) {
+        best = len;
+        bestd = ip1 - pc;
+        key = w32[ip1 + best - 1] >> 16;
+        if (best >= nice || best >= maxl) done = true;
+      }
+    }
+    if (has && done) {
+      store_walked();
+      has = false;
+    }
+#else
     // PB_STEPS hops along the 4-gram subsequence, branch-free; candidates passing the quick
     // test (bytes best - 1, best of the lagging best) are recorded
     uint32_t cand[PB_STEPS];
@@ -1449,6 +1496,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
       store_walked();
       has = false;
     }
+#endif
   }
 }
 
