@@ -790,22 +790,26 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
   __syncthreads();
   const uint32_t sw = (uint32_t)__cvta_generic_to_shared(w32);
 
-  for (uint64_t p0 = s; p0 < e; p0 += blockDim.x) {
-    const uint64_t p = p0 + threadIdx.x;
-    const uint32_t ip1 = (uint32_t)(p - wlo) + 1;
-    const uint32_t wp = p < e ? w32[ip1] : 0;
+  // positions as 1-based window indices (32-bit): ip1 = p - wlo + 1
+  const uint32_t nrel = (uint32_t)umin64(n - wlo, 1u << 30);
+  const uint32_t ie = (uint32_t)(e - wlo) + 1;  // ip1 < ie: p < e
+  const uint32_t ix0 = wlo == 0 ? 1u : 0u;     // the index of absolute position 0 (NIL), if in the window
+  uint2* profw = prof + L.pbase + wlo - 1;
+  for (uint32_t i0 = (uint32_t)(s - wlo) + 1; i0 < ie; i0 += blockDim.x) {
+    const uint32_t ip1 = i0 + threadIdx.x;
+    const bool inb = ip1 < ie;
+    const uint32_t wp = inb ? w32[ip1] : 0;
     const uint32_t c0 = wp & 0xffff;
     const uint32_t d0 = ip1 - c0;
-    const bool live = p < e && p + MIN_MATCH <= n && c0 != 0 && d0 <= MAX_DIST && wlo + c0 - 1 != 0;
+    const bool live = inb && ip1 + 2 <= nrel && c0 != 0 && d0 <= MAX_DIST && c0 != ix0;
     uint32_t best = MIN_MATCH - 1, bestd = 0, flag = 0, nice = 0, maxl = 0, lim1 = 0;
     // ic4: 4 x the candidate's 1-based window index (byte offset of its word)
     uint32_t ic4 = 0, key = PF_DEAD_KEY, offb = sw + 4 * (MIN_MATCH - 2) + 2;
     if (live) {
-      const uint32_t la = (uint32_t)umin64(n - p, 1u << 20);
+      const uint32_t la = min(nrel - ip1 + 1, 1u << 20);
       nice = min(NICE_LENGTH, la);
       maxl = min(MAX_MATCH, la);
-      const uint64_t limit = p > MAX_DIST ? p - MAX_DIST : 0;
-      lim1 = limit >= wlo ? (uint32_t)(limit - wlo) + 1 : 0;
+      lim1 = (uint32_t)max((int)ip1 - (int)MAX_DIST, 1);
       flag = d0 == MAX_DIST ? PROF_AT_MAXDIST : 0;
       ic4 = 4 * c0;
       key = (wp >> 16) | (w32[ip1 + best - 1] & 0xffff0000u);
@@ -813,7 +817,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     // zlib tests the limit only from the second candidate on (do ... while (prev > limit)):
     // a head exactly at MAX_DIST is still compared, and every later candidate is below it
     const uint32_t lim4 = 4 * lim1 - (live && c0 == lim1 ? 4u : 0u);
-    const uint32_t qw2 = p < e ? w32[ip1 + 2] : 0u;  // bytes p + 2, p + 3 (wlen covers e + 274)
+    const uint32_t qw2 = inb ? w32[ip1 + 2] : 0u;  // bytes p + 2, p + 3 (wlen covers e + 274)
 #ifndef PF_NO_HEAD_SEED
     // The head candidate (chain step 1) is extended exactly before the walk, so best starts at its
     // length: the batches' quick test then records only candidates that can beat it (with best = 2,
@@ -941,10 +945,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
 #endif
       batch(std::integral_constant<int, PF_B2>());
     }
-    if (p < e) {
+    if (inb) {
       // y: the 32-chain profile (the flag lives in x) | the byte before p << 24 for the parse
       const uint32_t yb = with_bytes ? (w32[ip1 - 1] << 8) & 0xff000000u : (live ? flag : 0u);
-      prof[L.pbase + p] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
+      profw[ip1] = make_uint2(live ? prof_pack(best, bestd) | flag : 0, (live ? r32 : 0u) | yb);
     }
   }
 }
