@@ -2217,21 +2217,17 @@ __device__ __forceinline__ void t_down_pf(uint32_t* heap, int heap_len, int k) {
   }
   heap[k] = v;
 }
+// (key(a) <= key(b) as a <= (b | 0x3ff): the node field never decides; heap[heap_len + 1] holds
+// a sentinel above every key, so a missing right son is never taken -- t_build_tree keeps it)
 __device__ __forceinline__ void t_down_plain(uint32_t* heap, int heap_len, int k) {
   const uint32_t v = heap[k];
-  const uint32_t vk = v >> 10;
   int j = k << 1;
   while (j <= heap_len) {
     const uint2 sons = *reinterpret_cast<const uint2*>(heap + j);
-    uint32_t hj = sons.x;
-    if (j < heap_len) {
-      const uint32_t hj1 = sons.y;
-      if ((hj1 >> 10) <= (hj >> 10)) {
-        j++;
-        hj = hj1;
-      }
-    }
-    if (vk <= (hj >> 10)) break;
+    const bool right = sons.y <= (sons.x | 0x3ffu);
+    const uint32_t hj = right ? sons.y : sons.x;
+    j += right;
+    if (v <= (hj | 0x3ffu)) break;
     heap[k] = hj;
     k = j;
     j <<= 1;
@@ -2269,11 +2265,13 @@ __device__ int t_build_tree(TreesState* s, TreeArr<ELEMS>* t) {
     if (KIND == 0) s->static_len -= c_z.sl_len[node];
     else if (KIND == 1) s->static_len -= 5;
   }
+  heap[heap_len + 1] = 0xffffffffu;  // t_down_plain's right-son sentinel
   for (n = heap_len / 2; n >= 1; n--) t_down<LAT>(heap, heap_len, n);
   node = ELEMS;
   do {
     const uint32_t en = heap[1];
     heap[1] = heap[heap_len--];
+    heap[heap_len + 1] = 0xffffffffu;
     t_down<LAT>(heap, heap_len, 1);
     const uint32_t em = heap[1];
     heap[--heap_max] = en;
