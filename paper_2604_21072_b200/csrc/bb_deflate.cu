@@ -2194,19 +2194,15 @@ __device__ __forceinline__ uint32_t t_depth(uint32_t e) { return (e >> 10) & 0x1
 // plain walk below serves that case.
 __device__ __forceinline__ void t_down_pf(uint32_t* heap, int heap_len, int k) {
   const uint32_t v = heap[k];
-  const uint32_t vk = v >> 10;
   int j = k << 1;
   if (j <= heap_len) {
     uint2 sons = *reinterpret_cast<const uint2*>(heap + j);  // j even: 8-byte aligned
     uint4 gs = *reinterpret_cast<const uint4*>(heap + 2 * j);  // 2j = 4k: 16-byte aligned
     for (;;) {
-      uint32_t hj = sons.x;
-      bool right = false;
-      if (j < heap_len && (sons.y >> 10) <= (hj >> 10)) {
-        right = true;
-        hj = sons.y;
-      }
-      if (vk <= (hj >> 10)) break;
+      // key comparisons and the right-son sentinel as in t_down_plain
+      const bool right = sons.y <= (sons.x | 0x3ffu);
+      const uint32_t hj = right ? sons.y : sons.x;
+      if (v <= (hj | 0x3ffu)) break;
       heap[k] = hj;
       k = j + right;
       j = k << 1;
