@@ -527,8 +527,13 @@ __device__ bool verify_dynamic(const uint8_t* p, uint64_t n, uint64_t b) {
       copy = 11 + r.take(7);
     }
     if (have + copy > nlen + ndist) return false;
+    if (!len) {  // zero lengths only advance the count (runs of up to 138: one step, not a loop)
+      have += copy;
+      prev = len;
+      if (r.past_end()) return false;
+      continue;
+    }
     for (uint32_t k = 0; k < copy; k++, have++) {
-      if (!len) continue;
       if (have < nlen) {
         kl += 32768u >> len;
         if (kl > 32768u) return false;
