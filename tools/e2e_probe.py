@@ -47,6 +47,38 @@ for _ in range(STEPS):
 torch.cuda.synchronize()
 print(f"(b2) the same with every step joined: {1e3 * (time.perf_counter() - t0) / STEPS:.2f} ms/step")
 
+# (b3) per step: all compresses over the threads, join, then all decompresses, join (the
+# multi-GPU step's shape: the length doorbell sits between the two phases)
+cbuf = [torch.empty(bound, dtype=torch.uint8, device="cuda") for _ in dev]
+dbuf = [torch.empty_like(d) for d in dev]
+clen = [0] * len(dev)
+sts = [torch.cuda.Stream() for _ in range(T)]
+
+
+def ph_c(t):
+    torch.cuda.set_device(0)
+    for k in range(t, len(dev), T):
+        clen[k] = dc.compress_into(dev[k], cbuf[k], stream=sts[t])
+    sts[t].synchronize()
+
+
+def ph_d(t):
+    torch.cuda.set_device(0)
+    for k in range(t, len(dev), T):
+        dc.decompress_into(cbuf[k][:clen[k]], dbuf[k], stream=sts[t])
+    sts[t].synchronize()
+
+
+list(ex.map(ph_c, range(T)))
+list(ex.map(ph_d, range(T)))
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(STEPS):
+    list(ex.map(ph_c, range(T)))
+    list(ex.map(ph_d, range(T)))
+torch.cuda.synchronize()
+print(f"(b3) compress phase then decompress phase, {T} threads each: {1e3 * (time.perf_counter() - t0) / STEPS:.2f} ms/step")
+
 outs = [torch.empty(bound, dtype=torch.uint8, device="cuda") for _ in dev]
 backs = [torch.empty_like(d) for d in dev]
 lens = dc.compress_batch(dev, outs)
