@@ -1513,6 +1513,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
 constexpr uint32_t K4S_CTAS = 4;  // x 256 threads = samples per lane
 static std::atomic<uint64_t> g_k4_positions[2];  // positions profiled by the classic walk / by K4G
 constexpr uint64_t K4G_MIN_LANE = 1u << 20;
+#ifndef K4G_MARGIN
+#define K4G_MARGIN 2  // K4G where L >= S4 + H4 + K4G_MARGIN (means per sampled position)
+#endif
 __global__ void __launch_bounds__(256) k_k4_sample(const LaneDev* __restrict__ lanes, const uint16_t* __restrict__ pd,
                                                    unsigned long long* __restrict__ stat) {
   const LaneDev L = lanes[blockIdx.y];
@@ -3336,9 +3339,13 @@ int deflate_containers(DeflateEngine* e, const std::vector<LaneJob>& jobs,
         if (rc) return rc;
         BB_CUDA_TRY(cudaMemcpyAsync(e->h_pinned, d_k4stat, 32ull * nl, cudaMemcpyDeviceToHost, st));
         BB_CUDA_TRY(cudaStreamSynchronize(st));
+        static const bool k4_debug = getenv("BB_K4_DEBUG") != nullptr;
         for (int i = 0; i < nl; i++) {
           const uint64_t* S = e->h_pinned + 4 * i;
-          use_g[i] = S[3] && S[0] >= 2 * (S[1] + S[2]) + 16 * S[3];
+          use_g[i] = S[3] && S[0] >= S[1] + S[2] + K4G_MARGIN * S[3];
+          if (k4_debug && S[3])
+            fprintf(stderr, "k4 lane %d n=%llu L=%.2f S4=%.2f H4=%.2f -> %s\n", i, (unsigned long long)L[i].n,
+                    (double)S[0] / S[3], (double)S[1] / S[3], (double)S[2] / S[3], use_g[i] ? "K4G" : "classic");
         }
       }
     }
