@@ -1509,7 +1509,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile4(const LaneDev* __res
 // candidate + 11 hops); on short chains (fp16 planes: ~6 steps, no 4-gram candidates) its
 // two passes cost more than K4's one.  A sampled walk per lane (1024 positions, K3 links in
 // global memory) measures the chain length L, the steps to the first same-4-gram candidate
-// S4 and the same-4-gram hops H4; the host picks K4G where L >= 2 (S4 + H4) + 16 on average.
+// S4 and the same-4-gram hops H4; the host picks K4G where L >= S4 + H4 + K4G_MARGIN on average
+// (K4G's one-load steps are cheaper than the classic walk's, its two passes cost a couple of
+// steps per position: config3's f32 planes with L = 35 / 119 gain, fp16 planes with L = 6 = S4 lose).
 constexpr uint32_t K4S_CTAS = 4;  // x 256 threads = samples per lane
 static std::atomic<uint64_t> g_k4_positions[2];  // positions profiled by the classic walk / by K4G
 constexpr uint64_t K4G_MIN_LANE = 1u << 20;
