@@ -192,3 +192,17 @@ def test_oracle_restatement_at_full_config2_size(oracle):
     c = oracle.compress(data, 1, True)
     assert len(c) == e["len"] == 47056924
     assert hashlib.sha256(c).hexdigest() == e["sha256"]
+
+
+def test_zlib_hash_keeps_all_of_a_trigram_but_z():
+    """K4G's k_gram4 compares chain candidates by z = the top three bits of bytes 0-2 (+ byte 3)
+    instead of the bytes themselves.  That is exact because zlib's 15-bit hash
+    ((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff, with z, determines the 3-gram: every entry of a
+    position's chain has its hash, so on a chain "same 3-gram" is "same z"."""
+    import numpy as np
+    b = np.arange(1 << 24, dtype=np.uint32)
+    b0, b1, b2 = b & 0xff, (b >> 8) & 0xff, b >> 16
+    h = ((b0 << 10) ^ (b1 << 5) ^ b2) & 0x7fff
+    z = (b0 >> 5) | ((b1 >> 5) << 3) | ((b2 >> 5) << 6)
+    key = (h << 9) | z  # injective on all 2^24 trigrams iff (hash, z) determines the trigram
+    assert np.unique(key).size == 1 << 24
