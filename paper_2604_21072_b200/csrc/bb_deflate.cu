@@ -707,7 +707,8 @@ constexpr uint32_t PF_DEAD_KEY = 0xffffffffu;
 __device__ unsigned long long g_pf_stats[4];  // flushes, recorded candidates, warp flush iterations, batches
 #endif
 #ifndef PF_B1
-#define PF_B1 8  // chain steps per batch within the first 32 (budget-32 snapshot)
+#define PF_B1 4  // chain steps per batch within the first 32 (budget-32 snapshot); 4 since the long
+                 // chains went to K4G (classic lanes walk ~1-6 steps: config4 K4 44.0 vs 44.7 ms at 8)
 #endif
 #ifndef PF_B2
 #define PF_B2 16  // chain steps per batch for candidates 33..128
@@ -818,7 +819,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) k_profile3(const LaneDev* __res
     // a head exactly at MAX_DIST is still compared, and every later candidate is below it
     const uint32_t lim4 = 4 * lim1 - (live && c0 == lim1 ? 4u : 0u);
     const uint32_t qw2 = inb ? w32[ip1 + 2] : 0u;  // bytes p + 2, p + 3 (wlen covers e + 274)
-#ifndef PF_NO_HEAD_SEED
+#ifdef PF_HEAD_SEED  // off since the long chains went to K4G: config4 K4 43.6 vs 44.7 ms, config2 2.37 vs 2.43
     // The head candidate (chain step 1) is extended exactly before the walk, so best starts at its
     // length: the batches' quick test then records only candidates that can beat it (with best = 2,
     // every same-3-gram candidate of the first batch was recorded and extended in the flush).  The
