@@ -227,6 +227,10 @@ __device__ __forceinline__ void hp_load_tile(const uint8_t* src, uint64_t n, uin
 #define HP4_SEG_OVR 32768
 #endif
 constexpr uint32_t HP4_SEG = HP4_SEG_OVR;
+// a position whose hash is new to its segment leaves HP_MARK | hash for k_hash_fix2 (in-segment
+// distances are < 0x8000, so the marker is unambiguous and fix-up needs no byte reloads)
+constexpr uint32_t HP_MARK = 0x8000u;
+static_assert(HP4_SEG <= 32768, "distances within a segment must stay below HP_MARK");
 constexpr int HP6_D = 8;
 
 __device__ __forceinline__ uint32_t hp_hash_at(uint32_t w, uint32_t x, int k, int lane) {
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(32) k_hash_prev6(const LaneDev* __restrict__ l
             d[k] = lane - (31 - __clz(lower));
           } else {
             const uint32_t r = head[h[k]];
-            d[k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
+            d[k] = r ? (uint32_t)(q - (s + r - 1)) : HP_MARK | h[k];  // resolve from the previous segment
           }
         }
         __syncwarp();
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(32 * HP7_W) k_hash_prev7(const LaneDev* __rest
             d[u][k] = lane - (31 - __clz(lower));
           } else {
             const uint32_t r = head[h[u][k]];
-            d[u][k] = r ? (uint32_t)(q - (s + r - 1)) : 0xffffu;  // 0xffff: resolve from the previous segment
+            d[u][k] = r ? (uint32_t)(q - (s + r - 1)) : HP_MARK | h[u][k];  // resolve from the previous segment
           }
         }
         __syncwarp();
@@ -558,7 +562,7 @@ __global__ void __launch_bounds__(32 * HP8_W) k_hash_prev8(const LaneDev* __rest
       for (int r = 0; r < 4; r++) {
         const uint32_t q = c + (key[u][r] & 127);
         uint32_t dd = d[u][r];
-        if ((fl[u] >> r) & 1) dd = hv[u][r] ? q + 1 - hv[u][r] : 0xffffu;  // 0xffff: the previous segment
+        if ((fl[u] >> r) & 1) dd = hv[u][r] ? q + 1 - hv[u][r] : HP_MARK | (key[u][r] >> 7);  // the previous segment
         if (q < se) out[q] = (uint16_t)dd;
       }
       cw[u] = nw[u], cx[u] = nx[u];
@@ -596,13 +600,12 @@ __global__ void __launch_bounds__(256) k_hash_fix2(const LaneDev* __restrict__ l
     bool any = false;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      if (v[k] != 0xffff) continue;
+      if (!(v[k] & HP_MARK)) continue;
       any = true;
       const uint64_t q = q0 + k;
       uint32_t d = 0;
       if (!first) {
-        const uint32_t h =
-            (((uint32_t)__ldg(src + q) << 10) ^ ((uint32_t)__ldg(src + q + 1) << 5) ^ __ldg(src + q + 2)) & 0x7fff;
+        const uint32_t h = v[k] & 0x7fffu;  // the position's hash, carried in the marker
         const uint32_t r = prev[h];
         if (r) {
           const uint64_t dd = q - ((s - HP4_SEG) + r - 1);
