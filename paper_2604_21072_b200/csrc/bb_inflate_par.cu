@@ -1488,6 +1488,21 @@ __global__ void k_lift(const uint32_t* __restrict__ prev, uint32_t* __restrict__
   cur[g] = a >= SENT_END ? a : prev[a];
 }
 
+// every lifting level in one CTA when the nodes fit in it (small streams: one launch instead of one
+// per level -- config1 has ~11 levels of a few hundred nodes)
+constexpr uint32_t LIFT1_MAX = 1024;
+__global__ void __launch_bounds__(LIFT1_MAX) k_lift_all(uint32_t* __restrict__ jump, uint32_t nnodes, int levels) {
+  const uint32_t g = threadIdx.x;
+  for (int k = 1; k < levels; k++) {
+    const uint32_t* prev = jump + (size_t)(k - 1) * nnodes;
+    if (g < nnodes) {
+      const uint32_t a = prev[g];
+      jump[(size_t)k * nnodes + g] = a >= SENT_END ? a : prev[a];
+    }
+    __syncthreads();  // level k is complete (and visible to the block) before level k + 1 reads it
+  }
+}
+
 
 __global__ void k_chain_len(const PJob* __restrict__ jobs, int njobs, const uint32_t* __restrict__ jump,
                             uint32_t nnodes, int levels, Chain* __restrict__ chains) {
@@ -2388,10 +2403,15 @@ int par_inflate(ParInflate* P, const std::vector<InflateJob>& jobs, cudaStream_t
   k_link<<<(nnodes + 255) / 256, 256, 0, st>>>(d_jobs, d_node_job, nnodes, d_nodes, d_dbm, d_dpre, d_sbm, d_spre,
                                                d_jump);
   BB_LAUNCH_CHECK();
-  for (int k = 1; k < levels; k++) {
-    k_lift<<<(nnodes + 255) / 256, 256, 0, st>>>(d_jump + (size_t)(k - 1) * nnodes, d_jump + (size_t)k * nnodes,
-                                                 nnodes);
+  if (nnodes <= LIFT1_MAX) {
+    if (levels > 1) k_lift_all<<<1, LIFT1_MAX, 0, st>>>(d_jump, nnodes, levels);
     BB_LAUNCH_CHECK();
+  } else {
+    for (int k = 1; k < levels; k++) {
+      k_lift<<<(nnodes + 255) / 256, 256, 0, st>>>(d_jump + (size_t)(k - 1) * nnodes, d_jump + (size_t)k * nnodes,
+                                                   nnodes);
+      BB_LAUNCH_CHECK();
+    }
   }
   k_chain_len<<<(nj + 63) / 64, 64, 0, st>>>(d_jobs, nj, d_jump, nnodes, levels, d_chains);
   BB_LAUNCH_CHECK();
