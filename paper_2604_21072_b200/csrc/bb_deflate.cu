@@ -2476,7 +2476,7 @@ __global__ void __launch_bounds__(NT) k_blocks(const LaneDev* __restrict__ lanes
                                                        uint32_t* __restrict__ hdr) {
   __shared__ TreesState S;
   __shared__ uint32_t hw_buf[HDR_BYTES / 4];
-  __shared__ uint32_t s_len_sum, s_last_len, s_hdr_bits;
+  __shared__ uint32_t s_len_sum, s_last_len, s_hdr_bits, s_stored;
   // symbol counts as packed u16 pairs (a block has <= 16383 symbols)
   constexpr int NW = NT / 32;
   __shared__ uint32_t h_l2w[NW][(L_CODES + 1) / 2], h_d2w[NW][(D_CODES + 1) / 2];
@@ -2566,29 +2566,38 @@ __global__ void __launch_bounds__(NT) k_blocks(const LaneDev* __restrict__ lanes
       if (S.blt.len[c_bl_order[max_blindex]] != 0) break;
     S.opt_len += 3 * ((uint64_t)max_blindex + 1) + 5 + 5 + 4;
     S.blmax = max_blindex;
-    // dynamic header (send_all_trees)
+    uint64_t opt_lenb = (S.opt_len + 3 + 7) >> 3;
+    uint64_t static_lenb = (S.static_len + 3 + 7) >> 3;
+    // A block k_layout will certainly store (_tr_flush_block's rule, with the block start provably
+    // still in the window: <= 32000 bytes and >= 262 symbols, hence bytes, after it -- see k_layout's
+    // buf_ok) needs no tree description, code tables or size sums (the mantissa planes' blocks).
+    const bool stored = s_len_sum <= 32000 && L.total - s1 >= 262 &&
+                        (uint64_t)s_len_sum + 4 <= umin64(opt_lenb, static_lenb);
     HdrWriter hw{hw_buf, 0};
-    hw.put((uint32_t)(S.lmax + 1 - 257), 5);
-    hw.put((uint32_t)(S.dmax + 1 - 1), 5);
-    hw.put((uint32_t)(max_blindex + 1 - 4), 4);
-    for (int r = 0; r < max_blindex + 1; r++) hw.put(S.blt.len[c_bl_order[r]], 3);
-    t_send_tree(&S, &S.lt, S.lmax, hw);
-    t_send_tree(&S, &S.dt, S.dmax, hw);
+    if (!stored) {  // dynamic header (send_all_trees)
+      hw.put((uint32_t)(S.lmax + 1 - 257), 5);
+      hw.put((uint32_t)(S.dmax + 1 - 1), 5);
+      hw.put((uint32_t)(max_blindex + 1 - 4), 4);
+      for (int r = 0; r < max_blindex + 1; r++) hw.put(S.blt.len[c_bl_order[r]], 3);
+      t_send_tree(&S, &S.lt, S.lmax, hw);
+      t_send_tree(&S, &S.dt, S.dmax, hw);
+    }
     BlockInfo bi;
     bi.sym0 = s0;
     bi.nsym = nsym;
     bi.stored_len = s_len_sum;
     bi.last_len = s_last_len;
-    uint64_t opt_lenb = (S.opt_len + 3 + 7) >> 3;
-    uint64_t static_lenb = (S.static_len + 3 + 7) >> 3;
     bi.opt_lenb = (uint32_t)umin64(opt_lenb, 0xffffffffu);
     bi.static_lenb = (uint32_t)umin64(static_lenb, 0xffffffffu);
     bi.hdr_bits = hw.bits;
+    bi.dyn_bits = bi.static_bits = 0;
     bi.valid = 1;
     info[slot] = bi;
     s_hdr_bits = hw.bits;
+    s_stored = stored;
   }
   __syncthreads();
+  if (s_stored) return;
   // codes to global; exact bit sizes: sum over codes of freq * (len + extra)
   BlockCodes* bc = codes + slot;
   // (freq of internal/forced nodes is irrelevant: only real symbols are counted)
